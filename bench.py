@@ -1,0 +1,408 @@
+"""Benchmark of the batched fp64 PCG hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one batched PCG solve (LKR preconditioner, eps_rank 1e-8) of a whole
+BASELINE configuration batch to the reference stop rule: config 3 by default
+(n = 128, 256 realizations, contrast {1,100}, corrector RHS, tol 1e-8).
+Inputs (cell contrasts, RHS) are seeded synthetic data with the reference's
+generator; 4.3 GB per vector, far above the 126 MB L2, so no L2 flush is needed.
+
+value  = DOF-iterations/s over all ranks (sum n^3 * iterations / max-over-ranks
+         device time of K steps).  Realizations/s is reported beside it.
+e2e    = the same metric through the reference-facing call with HOST buffers:
+         H2D of beta + f from pinned memory, the solve, D2H of u + reports.
+Multi-GPU (torchrun): realization sharding, weak scaling, no data-path collective.
+--impl reference: the reference algorithm on host cores (the CPU oracle port,
+oracle/checkerhom_oracle.py -- the reference is pure Python and cannot be
+compiled or shipped), process pool over all host threads, bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "PCG DOF-iterations/s (fp64) and realizations/s vs HBM roofline, 1/2/4/8 GPU"
+UNIT = "DOF-iterations/s"
+
+# (L, n0, lam, batch, tol, rhs) -- BASELINE.json configs (SURVEY §8d mapping)
+CONFIG_NAMES = {
+    1: "3D L=8 n0=4 (n=32) x1, lam=0.1 (a in {0.1,1}), corrector RHS, tol 1e-8",
+    2: "3D L=16 n0=4 (n=64) x64, lam=0.1, corrector RHS, tol 1e-8",
+    3: "3D L=32 n0=4 (n=128) x256, lam=0.01 (contrast 100), corrector RHS, tol 1e-8",
+    4: "3D L=64 n0=4 (n=256) x16, lam=0.1, Gaussian RHS, tol 1e-10",
+    5: "3D L=32 n0=16 (n=512) x1, lam=0.1, corrector RHS, tol 1e-8",
+}
+CFG = {
+    1: dict(L=8, n0=4, lam=0.1, batch=1, tol=1e-8, rhs="corrector"),
+    2: dict(L=16, n0=4, lam=0.1, batch=64, tol=1e-8, rhs="corrector"),
+    3: dict(L=32, n0=4, lam=0.01, batch=256, tol=1e-8, rhs="corrector"),
+    4: dict(L=64, n0=4, lam=0.1, batch=16, tol=1e-10, rhs="gaussian"),
+    5: dict(L=32, n0=16, lam=0.1, batch=1, tol=1e-8, rhs="corrector"),
+}
+
+# algorithmic HBM bytes per DOF per launch of each kernel class
+def kernel_bytes_per_dof(n):
+    spec = 8.0 * (n // 2 + 1) / (n // 2)  # half spectrum, complex128, per real DOF
+    return {
+        "stencil_dot": 8.0,                       # read p
+        "fwd_plane": 8.0 * 5 + spec,              # read p,u,r; write u,r; write S
+        "mid_column": 2.0 * spec,                 # read + write S
+        "inv_plane": spec + 16.0,                 # read S, read p, write p
+    }
+
+
+KERNEL_CLASSES = ["stencil_dot", "fwd_plane", "mid_column", "inv_plane"]
+B_ALG = 104.0  # SURVEY §8d algorithmic bytes per DOF-iteration (whole iteration)
+
+
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm = []
+        smax = None
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                smax = float(s[1])
+            except ValueError:
+                continue
+            for i, nm in enumerate(names):
+                if s[2 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_inputs(chk, orc_free_cfg, cfg_id, rank, per_rank, torch):
+    """Seeded synthetic realizations m = rank*per_rank + j (reference generator)."""
+    c = CFG[cfg_id]
+    lat = chk.LatticeConfig(d=3, L=c["L"], n0=c["n0"], alpha="1/2", lam=c["lam"])
+    ms = [rank * per_rank + j for j in range(per_rank)]
+    seeds = [chk.derive_seed(0, m) for m in ms]
+    beta = np.stack([chk.sample_realization(lat, s).beta_cells.ravel() for s in seeds])
+    A = chk.StiffnessBatch(lat, beta)
+    if c["rhs"] == "corrector":
+        F = chk.corrector_rhs_batched(A, 1)
+    else:
+        n = lat.n
+        F = torch.empty((per_rank, n ** 3), dtype=torch.float64, device="cuda")
+        for j, s in enumerate(seeds):
+            f = np.random.default_rng(s).standard_normal(n ** 3)
+            F[j].copy_(torch.from_numpy(f - f.mean()))
+    return lat, beta, A, F
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2007_06524_b200 as chk
+    from paper_2007_06524_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg_id = args.config
+    c = CFG[cfg_id]
+    per_rank = c["batch"]  # weak scaling: every rank solves one full config batch
+    lat, beta_np, A, F = make_inputs(chk, None, cfg_id, rank, per_rank, torch)
+    n = lat.n
+    nb = n ** 3
+    opts = chk.SolveOptions(tol=c["tol"], preconditioner="lkr", eps_rank=1e-8)
+    P = chk.make_preconditioner(3, n, opts)
+    U = torch.empty_like(F)
+    ws = chk.solver.Workspace()
+    lib = _lib.load()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_step():
+        res = chk.pcg_solve_batched(A, F, opts, P, out=U, record_history=False, workspace=ws)
+        return res
+
+    for _ in range(args.warmup):
+        res = one_step()
+    barrier()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    lib.chk_profile_enable(1)
+    stream = torch.cuda.current_stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    dof_its = 0
+    launches = 0
+    reals = 0
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        res = one_step()
+        dof_its += int(np.sum(res.iterations)) * nb
+        launches += res.launches
+        reals += per_rank
+        assert np.all(res.status == 0), "a realization did not converge"
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = float(ev0.elapsed_time(ev1))
+    prof_ms = (ctypes_array := np.zeros(5, dtype=np.float64))
+    prof_n = np.zeros(5, dtype=np.int64)
+    import ctypes
+
+    lib.chk_profile_read(prof_ms.ctypes.data_as(ctypes.c_void_p), prof_n.ctypes.data_as(ctypes.c_void_p))
+    lib.chk_profile_enable(0)
+    del ctypes_array
+
+    # --- e2e: reference-facing call with host buffers --------------------------
+    beta_h = torch.from_numpy(beta_np).pin_memory()
+    F_h = F.cpu().pin_memory()
+    U_h = torch.empty_like(F_h).pin_memory()
+    e2e_ms = []
+    for step in range(args.warmup + args.steps):
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        beta_d = beta_h.to(dev, non_blocking=True)
+        F_d = F_h.to(dev, non_blocking=True)
+        A_e = chk.StiffnessBatch(lat, beta_d)
+        res_e = chk.pcg_solve_batched(A_e, F_d, opts, P, out=U, record_history=False, workspace=ws)
+        U_h.copy_(U, non_blocking=True)
+        t1.record(stream)
+        barrier()
+        if step >= args.warmup:
+            e2e_ms.append(float(t0.elapsed_time(t1)))
+    e2e_dof_its = int(np.sum(res_e.iterations)) * nb  # identical inputs every step
+    h2d = beta_h.numel() * 8 + F_h.numel() * 8
+    d2h = U_h.numel() * 8 + per_rank * (4 + 8 + 4 + 4)
+
+    # --- max over ranks -------------------------------------------------------
+    tot = torch.tensor([ms, float(dof_its), float(reals), float(launches),
+                        float(np.mean(e2e_ms)), float(e2e_dof_its)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = tot.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm_ = tot.clone()
+        dist.all_reduce(sm_, op=dist.ReduceOp.SUM)
+        ms_max, e2e_max = float(mx[0]), float(mx[4])
+        dof_total, reals_total, launches_total, e2e_dof_total = float(sm_[1]), float(sm_[2]), float(sm_[3]), float(sm_[5])
+    else:
+        ms_max, e2e_max = ms, float(np.mean(e2e_ms))
+        dof_total, reals_total, launches_total, e2e_dof_total = float(dof_its), float(reals), float(launches), float(e2e_dof_its)
+
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        value = dof_total / (ms_max / 1e3)
+        per_kernel = {}
+        kb = kernel_bytes_per_dof(n)
+        dof_it_rank = dof_its  # rank 0's own work, for the live kernel figures
+        for i, name in enumerate(KERNEL_CLASSES):
+            if prof_n[i] == 0 or prof_ms[i] <= 0:
+                continue
+            achieved = kb[name] * dof_it_rank / (prof_ms[i] / 1e3) / 1e9
+            per_kernel[name] = {"ms_total": round(prof_ms[i], 3), "launches": int(prof_n[i]),
+                                "avg_us": round(1e3 * prof_ms[i] / prof_n[i], 2),
+                                "alg_bytes_per_dof": round(kb[name], 3),
+                                "achieved_gbs": round(achieved, 1),
+                                "frac": round(achieved / peak, 3),
+                                "share": round(prof_ms[i] / max(1e-9, prof_ms[:4].sum()), 3)}
+        dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_total"]) if per_kernel else None
+        traffic = None
+        prof_json = os.path.join(REPO, "profiles", "ncu_traffic.json")
+        if dom and os.path.exists(prof_json):
+            tj = json.load(open(prof_json)).get(f"config{cfg_id}", {})
+            traffic = tj.get(dom)
+        roofline = None
+        if dom:
+            d = per_kernel[dom]
+            roofline = {"bound": "hbm", "kernel": dom, "achieved": d["achieved_gbs"], "peak": peak,
+                        "peak_kind": peak_kind, "unit": "GB/s", "frac": d["frac"],
+                        "traffic": traffic,
+                        "alg_bytes_per_dof": d["alg_bytes_per_dof"],
+                        "iteration_frac_104B": round(value / world * B_ALG / 1e9 / peak, 3)}
+        cpu = cpu_baseline(cfg_id) if (world == 1 and not args.no_cpu_baseline) else None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference seeded generator: derive_seed(0,m), Philox cells, corrector/Gaussian RHS)",
+            "config": {"workload": f"config{cfg_id}: {CONFIG_NAMES[cfg_id]}", "n": n,
+                       "realizations_per_gpu": per_rank, "preconditioner": "lkr eps_rank=1e-8",
+                       "parallelism": f"realization sharding x{world}",
+                       "l2": "inputs 8*n^3*B bytes per vector >> 126 MB L2 (no flush needed)"},
+            "realizations_per_s": reals_total / (ms_max / 1e3),
+            "dof_iterations": dof_total,
+            "roofline": roofline,
+            "kernels": per_kernel,
+            "e2e": {"value": e2e_dof_total / (e2e_max / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+                    "ms_per_step": e2e_max},
+            "gpu_launches": int(launches_total),
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference algorithm (oracle port) on host cores
+# ---------------------------------------------------------------------------
+
+
+def _cpu_solve(cfg_id, m):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from threadpoolctl import threadpool_limits
+
+    from oracle import checkerhom_oracle as orc
+
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        beta, F, f = orc.config_problem(cfg_id, m)
+        fac = _cpu_solve.fac.get(cfg_id) if hasattr(_cpu_solve, "fac") else None
+        if fac is None:
+            fac = orc.lkr_factors(F.shape[0])
+            _cpu_solve.fac = getattr(_cpu_solve, "fac", {})
+            _cpu_solve.fac[cfg_id] = fac
+        dg = orc.lkr_diagonal(fac)
+        A = orc.StencilMatrix(F, CFG[cfg_id]["lam"])
+        t1 = time.perf_counter()
+        u, rep = orc.pcg_solve(A.__matmul__, f, lambda x: orc.apply_lkr(fac, x, dg), tol=CFG[cfg_id]["tol"])
+        t2 = time.perf_counter()
+    return rep.iterations, F.shape[0] ** 3, t2 - t1, t1 - t0
+
+
+def cpu_baseline(cfg_id):
+    """Single-core oracle solve of realization 0 of the workload (bounded sample)."""
+    its, nb, t_solve, t_setup = _cpu_solve(cfg_id, 0)
+    return {"value": its * nb / t_solve, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"config{cfg_id} realization m=0: full PCG solve ({its} iterations) with the "
+                      f"numpy oracle (oracle/checkerhom_oracle.py), 1 thread, {t_solve:.1f} s"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from concurrent.futures import ProcessPoolExecutor
+
+    cfg_id = args.config
+    c = CFG[cfg_id]
+    n = c["n0"] * c["L"]
+    per_worker_gb = 0.5 * (n / 128) ** 3 + 0.2
+    try:
+        import psutil
+
+        mem_gb = psutil.virtual_memory().available / 2 ** 30
+    except Exception:  # noqa: BLE001
+        mem_gb = 64.0
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, c["batch"], int(mem_gb * 0.6 / per_worker_gb)))
+    rates = []
+    m_next = 0
+    with ProcessPoolExecutor(max_workers=workers) as pool:
+        for step in range(args.warmup + args.steps):
+            ms = list(range(m_next, m_next + workers))
+            m_next += workers
+            t0 = time.perf_counter()
+            out = list(pool.map(_cpu_solve, [cfg_id] * workers, [m % c["batch"] for m in ms]))
+            dt = time.perf_counter() - t0
+            if step >= args.warmup:
+                rates.append(sum(o[0] * o[1] for o in out) / dt)
+    value = float(np.mean(rates))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "impl": "reference", "data": "synthetic (same generator as our arm)",
+            "config": {"workload": f"config{cfg_id}: {CONFIG_NAMES[cfg_id]}", "n": n},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                             "sample": f"per step {workers} realizations of config{cfg_id} solved to the "
+                                       f"reference stop rule, one per process (pattern of "
+                                       f"homogenize.py:149-161), 1 BLAS thread each"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CFG))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

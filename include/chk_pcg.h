@@ -1,0 +1,153 @@
+/*
+ * chk_pcg.h -- C ABI of the B200-native PCG hot path for the periodic 3-D
+ * checkerboard problem of arXiv 2007.06524 (reference package `checkerhom`,
+ * /root/reference/pkg/src/checkerhom).
+ *
+ * Plain pointers and sizes only.  All double arrays passed to the compute
+ * entry points are DEVICE pointers (cudaMalloc / torch CUDA tensors) unless a
+ * comment says "host".  Grid vectors are fp64, C order, axis 0 slowest
+ * (operators.py:374-381): idx = (x0*n + x1)*n + x2.  A batch of B
+ * realizations is stored back to back ([B][n^3]).  `stream` is a
+ * cudaStream_t (NULL = legacy default stream); every call is stream-ordered
+ * with respect to it.
+ *
+ * Return codes (mirroring the reference error taxonomy, errors.py:4-38):
+ *   CHK_OK           0
+ *   CHK_EINVAL       1  bad argument / size mismatch      -> ValueError
+ *                       (operators.py:304-305, spectral.py:107-108, lowrank.py:187-188)
+ *   CHK_EUNSUPPORTED 2  unsupported grid (d != 3, n not a power of two in
+ *                       [8, 512])                        -> ValueError
+ *   CHK_ECUDA        3  CUDA runtime failure              -> RuntimeError
+ * chk_last_error() returns a thread-local message for the last failure.
+ *
+ * Per-realization PCG status (PcgReport semantics, solver.py:61-70,161-194):
+ *   CHK_CONVERGED 0, CHK_NOT_CONVERGED 1, CHK_BREAKDOWN 2 (-> SolverBreakdown,
+ *   solver.py:164-165,172-173).
+ */
+#ifndef CHK_PCG_H
+#define CHK_PCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHK_OK 0
+#define CHK_EINVAL 1
+#define CHK_EUNSUPPORTED 2
+#define CHK_ECUDA 3
+
+#define CHK_CONVERGED 0
+#define CHK_NOT_CONVERGED 1
+#define CHK_BREAKDOWN 2
+
+/* Preconditioner kinds (solver.py:29 PRECONDITIONERS). */
+#define CHK_PRECOND_FOURIER 0     /* exact pseudo-inverse, spectral.py:77-87,98-112 */
+#define CHK_PRECOND_LKR 1         /* low Kronecker rank, lowrank.py:141-192 */
+#define CHK_PRECOND_REGULARIZED 2 /* 1/(g+delta), spectral.py:90-95 */
+
+/* Grid / lattice geometry of one realization batch (lattice.py:82-166).
+ * n = n0*L; k = 2*alpha*n0 h-cells of the sub-cell per axis, starting at
+ * `offset` inside each cell; lam = background conductivity lambda. */
+typedef struct chk_grid {
+  int32_t d;      /* must be 3 */
+  int32_t n;      /* grid nodes per axis */
+  int32_t L;      /* cells per axis */
+  int32_t n0;     /* h-cells per cell (power of two >= 4) */
+  int32_t k;      /* sub-cell width in h-cells */
+  int32_t offset; /* sub-cell start inside its cell */
+  double lam;     /* lambda in (0, 1] */
+} chk_grid;
+
+typedef struct chk_precond_plan chk_precond_plan; /* opaque, immutable after create */
+
+/* Options of one batched solve (SolveOptions, solver.py:32-58). */
+typedef struct chk_pcg_opts {
+  double tol;
+  int32_t max_iter;
+  int32_t precond_residual_stopping; /* solver.py:181-183 */
+} chk_pcg_opts;
+
+int32_t chk_abi_version(void);
+const char* chk_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Stiffness matvec: y = A x for B realizations (replaces the CSR product
+ * `A.matrix() @ x`, solver.py:150,162 / operators.py:122-131, equal to the
+ * edge-weighted stencil of tests/oracles.py:35-82).
+ *   beta : device [B][L^3] per-cell contrast (0 for uncovered cells)
+ *   x, y : device [B][n^3]
+ *   xy   : device [B] receives <x, y> (p'Ap of solver.py:163) or NULL
+ * ------------------------------------------------------------------------- */
+int32_t chk_stencil_apply(const chk_grid* grid, const double* beta, const double* x, double* y,
+                          double* xy, int32_t B, void* stream);
+
+/* Corrector right-hand side on the device: f = scale * 1/2 (c[x+e_i] - c[x-e_i])
+ * with c the nodal 2^3-cell average of the cell field (homogenize.py:75-89,
+ * lattice.py:326-345).  direction in {1,2,3}; scale = h^(d-1) reproduces
+ * corrector_rhs, h^(d-1)*h^(2-d) = h the PCG load of homogenize.py:110. */
+int32_t chk_corrector_rhs(const chk_grid* grid, const double* beta, double* f, int32_t B,
+                          int32_t direction, double scale, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Preconditioner plans (replace _cached_preconditioner, solver.py:79-93).
+ * factors: HOST [3][r1][n] fp64, the CanonicalTensor factors produced by
+ * dc_correction(canonical_reciprocal(...)) (lowrank.py:129,147-180), consumed
+ * as-is; only read for CHK_PRECOND_LKR (pass NULL/0 otherwise).
+ * eigenvalues: HOST [n], fourier_eigenvalues(n).values (spectral.py:56-68);
+ * read for FOURIER / REGULARIZED (may be NULL for LKR).
+ * ------------------------------------------------------------------------- */
+int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const double* factors,
+                                const double* eigenvalues, double delta,
+                                chk_precond_plan** out);
+int32_t chk_precond_plan_destroy(chk_precond_plan* plan);
+
+/* Device workspace (bytes) a chk_precond_apply of B vectors needs. */
+size_t chk_precond_workspace_bytes(const chk_precond_plan* plan, int32_t B);
+
+/* z = Re ifftn(D * fftn(r)) for B vectors (apply_lkr_preconditioner,
+ * lowrank.py:183-192, and apply_fourier_preconditioner, spectral.py:98-112).
+ * The zero-frequency term is kept exactly as the reference computes it. */
+int32_t chk_precond_apply(const chk_precond_plan* plan, const double* r, double* z, int32_t B,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Batched mean-projected PCG (pcg_solve, solver.py:118-194), B independent
+ * realizations sharing one grid shape and one preconditioner.
+ *   beta       device [B][L^3]
+ *   f          device [B][n^3]   right-hand sides (not modified)
+ *   u          device [B][n^3]   solutions (output, mean zero)
+ *   iterations HOST   [B]        PcgReport.iterations
+ *   final_rel  HOST   [B]        PcgReport.final_residual
+ *   status     HOST   [B]        CHK_CONVERGED / CHK_NOT_CONVERGED / CHK_BREAKDOWN
+ *   rhs_projected HOST [B]       PcgReport.rhs_projected
+ *   history    HOST   [B][max_iter] relative residuals (PcgReport.residuals) or NULL
+ *   workspace  device buffer of chk_pcg_workspace_bytes(...) bytes
+ * The call returns after the solve completed (it synchronizes internally on
+ * a convergence poll every few iterations).
+ * ------------------------------------------------------------------------- */
+size_t chk_pcg_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, int32_t B,
+                               int32_t max_iter);
+int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan,
+                              const double* beta, const double* f, double* u, int32_t B,
+                              const chk_pcg_opts* opts, int32_t* iterations, double* final_rel,
+                              int32_t* status, int32_t* rhs_projected, double* history,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* Number of kernels launched by the last chk_pcg_solve_batched on this thread
+ * (the bench's gpu_launches evidence). */
+int64_t chk_last_launch_count(void);
+
+/* Per-kernel-class device timing (CUDA events on the launching stream) for the
+ * calling thread: classes 0 stencil_dot, 1 fwd_plane, 2 mid_column,
+ * 3 inv_plane, 4 other.  Enabling resets the accumulators; read returns the
+ * summed milliseconds and launch counts of the solves since. */
+int32_t chk_profile_enable(int32_t on);
+int32_t chk_profile_read(double* ms /* [5] */, int64_t* launches /* [5] */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHK_PCG_H */

@@ -1,0 +1,551 @@
+// chk_capi.cu -- C ABI (include/chk_pcg.h) over the sm_100a kernels.
+//
+// Host-side orchestration of the batched PCG (pcg_solve, solver.py:118-194):
+// init reductions, one preconditioner apply, then four kernels per iteration;
+// convergence is decided on the device, the host only polls a per-realization
+// status word every few iterations while the next iterations are already queued.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/chk_pcg.h"
+#include "chk_kernels.cuh"
+
+using namespace chk;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local long long g_launches = 0;
+
+// Optional per-kernel-class timing with CUDA events on the launching stream
+// (the bench's live roofline numbers).  Classes: 0 stencil_dot, 1 fwd_plane,
+// 2 mid_column, 3 inv_plane, 4 other.
+struct Profiler {
+  bool on = false;
+  double ms[5] = {0, 0, 0, 0, 0};
+  long long count[5] = {0, 0, 0, 0, 0};
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> open;
+  cudaEvent_t take() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void collect() {  // call after the stream synchronized
+    for (auto& o : open) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, o.second.first, o.second.second) == cudaSuccess) {
+        ms[o.first] += t;
+        count[o.first] += 1;
+      }
+      pool.push_back(o.second.first);
+      pool.push_back(o.second.second);
+    }
+    open.clear();
+  }
+};
+thread_local Profiler g_prof;
+
+struct ProfScope {
+  int kind;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  ProfScope(int k, cudaStream_t st) : kind(k), s(st) {
+    if (g_prof.on) {
+      a = g_prof.take();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = g_prof.take();
+      cudaEventRecord(b, s);
+      g_prof.open.push_back({kind, {a, b}});
+    }
+  }
+};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CHK_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) return fail(CHK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CHK_LAUNCHED()                                                               \
+  do {                                                                              \
+    ++g_launches;                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                            \
+    if (e_ != cudaSuccess) return fail(CHK_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Tile geometry per grid size: G interleaved x1 groups per plane slab, W
+// spectral columns per middle-pass tile.
+template <int N>
+struct Cfg;
+template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8;  };
+template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16; };
+template <> struct Cfg<32>  { static constexpr int G = 1,  W = 32; };
+template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16; };
+template <> struct Cfg<128> { static constexpr int G = 2,  W = 16; };
+template <> struct Cfg<256> { static constexpr int G = 8,  W = 2;  };
+template <> struct Cfg<512> { static constexpr int G = 16, W = 1;  };
+
+template <int N>
+struct Ops {
+  static constexpr int G = Cfg<N>::G, W = Cfg<N>::W, NR = N / G, H = N / 2 + 1;
+  static constexpr int TILES = NR * H / W;
+  static constexpr int PLANE_BLOCKS = N * G;  // per realization
+  static constexpr size_t plane_smem() { return (size_t)NR * H * sizeof(double2); }
+  static size_t mid_smem(int r1) {
+    return (size_t)N * (G * W + 1) * sizeof(double2) + (size_t)r1 * G * W * sizeof(double);
+  }
+  static int maxblk() { return PLANE_BLOCKS > TILES ? PLANE_BLOCKS : TILES; }
+
+  template <class K>
+  static cudaError_t allow_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+      return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return cudaSuccess;
+  }
+
+  static int fwd(int mode, cudaStream_t s, int B, Geo g, const double* beta, const double* src,
+                 double* u, double* r, double2* S, PlanDev pl, SolveCtl ctl, int it) {
+    const size_t sm = plane_smem();
+    dim3 grid(B * PLANE_BLOCKS), block(256);
+    ProfScope ps(1, s);
+    if (mode == FWD_APPLY) {
+      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_APPLY>, sm));
+      fwd_plane_kernel<N, G, FWD_APPLY><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+    } else if (mode == FWD_INIT) {
+      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_INIT>, sm));
+      fwd_plane_kernel<N, G, FWD_INIT><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+    } else {
+      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_ITER>, sm));
+      fwd_plane_kernel<N, G, FWD_ITER><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+    }
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
+  static int mid(int mode, cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it) {
+    const size_t sm = mid_smem(pl.kind == KIND_LKR ? pl.r1 : 0);
+    dim3 grid(B * TILES), block(256);
+    ProfScope ps(2, s);
+    if (mode == MID_APPLY) {
+      CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, MID_APPLY>, sm));
+      mid_column_kernel<N, G, W, MID_APPLY><<<grid, block, sm, s>>>(S, pl, ctl, it);
+    } else {
+      CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, MID_PCG>, sm));
+      mid_column_kernel<N, G, W, MID_PCG><<<grid, block, sm, s>>>(S, pl, ctl, it);
+    }
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
+  static int inv(int mode, cudaStream_t s, int B, const double2* S, double* out, PlanDev pl,
+                 SolveCtl ctl, int it) {
+    const size_t sm = plane_smem();
+    dim3 grid(B * PLANE_BLOCKS), block(256);
+    ProfScope ps(3, s);
+    if (mode == INV_APPLY) {
+      CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_APPLY>, sm));
+      inv_plane_kernel<N, G, INV_APPLY><<<grid, block, sm, s>>>(S, out, pl, ctl, it);
+    } else {
+      CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_PCG>, sm));
+      inv_plane_kernel<N, G, INV_PCG><<<grid, block, sm, s>>>(S, out, pl, ctl, it);
+    }
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
+  static int dot(cudaStream_t s, int B, Geo g, const double* beta, const double* p, SolveCtl ctl,
+                 int it) {
+    ProfScope ps(0, s);
+    stencil_dot_kernel<N, G><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, p, ctl, it);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
+  static int stencil(cudaStream_t s, int B, Geo g, const double* beta, const double* x, double* y,
+                     double* xy, double* part, unsigned* cnt) {
+    stencil_apply_kernel<N, G><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, x, y, xy, part, cnt);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
+  static int rhs_stats(cudaStream_t s, int B, const double* f, SolveCtl ctl) {
+    rhs_stats_kernel<N, G><<<B * PLANE_BLOCKS, 256, 0, s>>>(f, ctl);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
+  static int mean_u(cudaStream_t s, int B, const double* u, SolveCtl ctl) {
+    mean_u_kernel<N, G><<<B * PLANE_BLOCKS, 256, 0, s>>>(u, ctl);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
+  static int rhs(cudaStream_t s, int B, Geo g, const double* beta, double* f, int axis, double scale) {
+    dim3 grid(296, B);
+    corrector_rhs_kernel<N><<<grid, 256, 0, s>>>(g, beta, f, axis, scale);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
+};
+
+#define CHK_DISPATCH(n, EXPR)                       \
+  switch (n) {                                      \
+    case 8:   { using O = Ops<8>;   EXPR; } break;  \
+    case 16:  { using O = Ops<16>;  EXPR; } break;  \
+    case 32:  { using O = Ops<32>;  EXPR; } break;  \
+    case 64:  { using O = Ops<64>;  EXPR; } break;  \
+    case 128: { using O = Ops<128>; EXPR; } break;  \
+    case 256: { using O = Ops<256>; EXPR; } break;  \
+    case 512: { using O = Ops<512>; EXPR; } break;  \
+    default: return fail(CHK_EUNSUPPORTED, "unsupported n " + std::to_string(n)); \
+  }
+
+bool supported_n(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
+
+int maxblk_of(int n) {
+  int m = 0;
+  switch (n) {
+    case 8: m = Ops<8>::maxblk(); break;
+    case 16: m = Ops<16>::maxblk(); break;
+    case 32: m = Ops<32>::maxblk(); break;
+    case 64: m = Ops<64>::maxblk(); break;
+    case 128: m = Ops<128>::maxblk(); break;
+    case 256: m = Ops<256>::maxblk(); break;
+    case 512: m = Ops<512>::maxblk(); break;
+  }
+  return m;
+}
+
+int check_grid(const chk_grid* g, Geo* out) {
+  if (!g) return fail(CHK_EINVAL, "grid is NULL");
+  if (g->d != 3) return fail(CHK_EUNSUPPORTED, "only d = 3 is implemented on the GPU path");
+  if (!supported_n(g->n)) return fail(CHK_EUNSUPPORTED, "n must be a power of two in [8, 512]");
+  if (g->n0 < 1 || (g->n0 & (g->n0 - 1)) || g->L < 1 || g->n0 * g->L != g->n)
+    return fail(CHK_EINVAL, "need n = n0 * L with n0 a power of two");
+  if (g->k < 1 || g->k > g->n0 || g->offset < 0 || g->offset + g->k > g->n0)
+    return fail(CHK_EINVAL, "sub-cell window outside the cell");
+  if (!(g->lam > 0.0)) return fail(CHK_EINVAL, "lambda must be positive");
+  int sh = 0;
+  while ((1 << sh) < g->n0) ++sh;
+  *out = Geo{g->n, g->L, sh, g->n0 - 1, g->k, g->offset, g->lam};
+  return CHK_OK;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Workspace {
+  double* p;
+  double* r;
+  double2* S;
+  double* part;
+  RState* st;
+  double* hist;
+  size_t bytes;
+};
+
+Workspace carve(void* base, int n, int B, int max_iter) {
+  const size_t nb = (size_t)n * n * n;
+  const size_t spec = (size_t)n * n * (n / 2 + 1);
+  char* c = static_cast<char*>(base);
+  Workspace w{};
+  size_t off = 0;
+  w.p = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * nb * B);
+  w.r = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * nb * B);
+  w.S = reinterpret_cast<double2*>(c + off); off = align_up(off + sizeof(double2) * spec * B);
+  w.part = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * 2 * (size_t)maxblk_of(n) * B);
+  w.st = reinterpret_cast<RState*>(c + off); off = align_up(off + sizeof(RState) * B);
+  w.hist = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * (size_t)max_iter * B);
+  w.bytes = off;
+  return w;
+}
+
+struct PinnedStates {
+  RState* h = nullptr;
+  size_t cap = 0;
+  ~PinnedStates() {
+    if (h) cudaFreeHost(h);
+  }
+  RState* get(size_t n) {
+    if (n > cap) {
+      if (h) cudaFreeHost(h);
+      h = nullptr;
+      if (cudaMallocHost(&h, n * sizeof(RState)) != cudaSuccess) {
+        h = nullptr;
+        cap = 0;
+        return nullptr;
+      }
+      cap = n;
+    }
+    return h;
+  }
+};
+thread_local PinnedStates g_pinned;
+
+}  // namespace
+
+struct chk_precond_plan {
+  int kind;
+  int n;
+  int r1;
+  double delta;
+  double2* d_tw;
+  double* d_U;
+  double* d_lam;
+};
+
+static PlanDev plan_dev(const chk_precond_plan* p) {
+  return PlanDev{p->d_tw, p->d_U, p->d_lam, p->r1, p->kind, p->delta};
+}
+
+extern "C" {
+
+int32_t chk_abi_version(void) { return 1; }
+const char* chk_last_error(void) { return g_err.c_str(); }
+int64_t chk_last_launch_count(void) { return g_launches; }
+
+int32_t chk_profile_enable(int32_t on) {
+  g_prof.collect();
+  g_prof.on = on != 0;
+  for (int i = 0; i < 5; ++i) {
+    g_prof.ms[i] = 0.0;
+    g_prof.count[i] = 0;
+  }
+  return CHK_OK;
+}
+
+int32_t chk_profile_read(double* ms, int64_t* launches) {
+  g_prof.collect();
+  for (int i = 0; i < 5; ++i) {
+    if (ms) ms[i] = g_prof.ms[i];
+    if (launches) launches[i] = g_prof.count[i];
+  }
+  return CHK_OK;
+}
+
+int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const double* factors,
+                                const double* eigenvalues, double delta, chk_precond_plan** out) {
+  if (!out) return fail(CHK_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!supported_n(n)) return fail(CHK_EUNSUPPORTED, "n must be a power of two in [8, 512]");
+  if (kind != CHK_PRECOND_LKR && kind != CHK_PRECOND_FOURIER && kind != CHK_PRECOND_REGULARIZED)
+    return fail(CHK_EINVAL, "unknown preconditioner kind");
+  if (kind == CHK_PRECOND_LKR && (factors == nullptr || r1 < 1 || r1 > 512))
+    return fail(CHK_EINVAL, "LKR plan needs factors [3][r1][n] with 1 <= r1 <= 512");
+  if (kind != CHK_PRECOND_LKR && eigenvalues == nullptr)
+    return fail(CHK_EINVAL, "Fourier plans need the eigenvalues");
+  if (kind == CHK_PRECOND_REGULARIZED && delta < 0.0) return fail(CHK_EINVAL, "delta must be >= 0");
+  auto* p = new chk_precond_plan{kind, n, kind == CHK_PRECOND_LKR ? r1 : 0, delta, nullptr, nullptr, nullptr};
+  // twiddles w[k] = exp(-2 pi i k / n), octant-reduced for symmetric accuracy
+  std::vector<double2> tw(n);
+  for (int k = 0; k < n; ++k) {
+    // angle = 2 pi k / n; use the exactly representable fraction k/n
+    long double a = 2.0L * 3.14159265358979323846264338327950288L * (long double)k / (long double)n;
+    tw[k] = make_double2((double)cosl(a), (double)(-sinl(a)));
+  }
+  // exact values at the quadrant points
+  tw[0] = make_double2(1.0, 0.0);
+  if (n % 4 == 0) {
+    tw[n / 4] = make_double2(0.0, -1.0);
+    tw[n / 2] = make_double2(-1.0, 0.0);
+    tw[3 * n / 4] = make_double2(0.0, 1.0);
+  }
+  cudaError_t e;
+  if ((e = cudaMalloc(&p->d_tw, sizeof(double2) * n)) != cudaSuccess) goto cuda_fail;
+  if ((e = cudaMemcpy(p->d_tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice)) != cudaSuccess) goto cuda_fail;
+  if (kind == CHK_PRECOND_LKR) {
+    if ((e = cudaMalloc(&p->d_U, sizeof(double) * 3 * (size_t)r1 * n)) != cudaSuccess) goto cuda_fail;
+    if ((e = cudaMemcpy(p->d_U, factors, sizeof(double) * 3 * (size_t)r1 * n, cudaMemcpyHostToDevice)) != cudaSuccess) goto cuda_fail;
+  } else {
+    if ((e = cudaMalloc(&p->d_lam, sizeof(double) * n)) != cudaSuccess) goto cuda_fail;
+    if ((e = cudaMemcpy(p->d_lam, eigenvalues, sizeof(double) * n, cudaMemcpyHostToDevice)) != cudaSuccess) goto cuda_fail;
+  }
+  *out = p;
+  return CHK_OK;
+cuda_fail:
+  chk_precond_plan_destroy(p);
+  return fail(CHK_ECUDA, std::string("plan create: ") + cudaGetErrorString(e));
+}
+
+int32_t chk_precond_plan_destroy(chk_precond_plan* p) {
+  if (!p) return CHK_OK;
+  if (p->d_tw) cudaFree(p->d_tw);
+  if (p->d_U) cudaFree(p->d_U);
+  if (p->d_lam) cudaFree(p->d_lam);
+  delete p;
+  return CHK_OK;
+}
+
+size_t chk_precond_workspace_bytes(const chk_precond_plan* p, int32_t B) {
+  if (!p || B < 1) return 0;
+  const size_t n = p->n;
+  return align_up(sizeof(double2) * n * n * (n / 2 + 1) * (size_t)B);
+}
+
+int32_t chk_precond_apply(const chk_precond_plan* p, const double* r, double* z, int32_t B,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  if (!p || !r || !z || B < 1) return fail(CHK_EINVAL, "bad arguments");
+  if (!workspace || workspace_bytes < chk_precond_workspace_bytes(p, B))
+    return fail(CHK_EINVAL, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double2* S = static_cast<double2*>(workspace);
+  PlanDev pl = plan_dev(p);
+  SolveCtl ctl{};
+  Geo g{};
+  g.n = p->n;
+  int rc = CHK_OK;
+  CHK_DISPATCH(p->n, {
+    rc = O::fwd(FWD_APPLY, s, B, g, nullptr, r, nullptr, nullptr, S, pl, ctl, 0);
+    if (rc) return rc;
+    rc = O::mid(MID_APPLY, s, B, S, pl, ctl, 0);
+    if (rc) return rc;
+    rc = O::inv(INV_APPLY, s, B, S, z, pl, ctl, 0);
+  });
+  return rc;
+}
+
+int32_t chk_stencil_apply(const chk_grid* grid, const double* beta, const double* x, double* y,
+                          double* xy, int32_t B, void* stream) {
+  Geo g;
+  int rc = check_grid(grid, &g);
+  if (rc) return rc;
+  if (!beta || !x || !y || B < 1) return fail(CHK_EINVAL, "bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* part = nullptr;
+  unsigned* cnt = nullptr;
+  if (xy) {
+    const size_t pb = sizeof(double) * 2 * (size_t)grid->n * 16 * B;  // N*G <= 16 n
+    CHK_CUDA(cudaMallocAsync(&part, pb + sizeof(unsigned) * B, s));
+    cnt = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(part) + pb);
+    CHK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * B, s));
+  }
+  CHK_DISPATCH(grid->n, { rc = O::stencil(s, B, g, beta, x, y, xy, part, cnt); });
+  if (part) CHK_CUDA(cudaFreeAsync(part, s));
+  return rc;
+}
+
+int32_t chk_corrector_rhs(const chk_grid* grid, const double* beta, double* f, int32_t B,
+                          int32_t direction, double scale, void* stream) {
+  Geo g;
+  int rc = check_grid(grid, &g);
+  if (rc) return rc;
+  if (!beta || !f || B < 1) return fail(CHK_EINVAL, "bad arguments");
+  if (direction < 1 || direction > 3) return fail(CHK_EINVAL, "direction must be in 1..3");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CHK_DISPATCH(grid->n, { rc = O::rhs(s, B, g, beta, f, direction - 1, scale); });
+  return rc;
+}
+
+size_t chk_pcg_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, int32_t B,
+                               int32_t max_iter) {
+  if (!grid || !plan || B < 1 || max_iter < 1 || !supported_n(grid->n)) return 0;
+  return carve(nullptr, grid->n, B, max_iter).bytes;
+}
+
+int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan,
+                              const double* beta, const double* f, double* u, int32_t B,
+                              const chk_pcg_opts* opts, int32_t* iterations, double* final_rel,
+                              int32_t* status, int32_t* rhs_projected, double* history,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  Geo g;
+  int rc = check_grid(grid, &g);
+  if (rc) return rc;
+  if (!plan || plan->n != grid->n) return fail(CHK_EINVAL, "plan grid size does not match");
+  if (!beta || !f || !u || B < 1 || !opts) return fail(CHK_EINVAL, "bad arguments");
+  if (!(opts->tol > 0.0)) return fail(CHK_EINVAL, "tolerance must be positive");
+  if (opts->max_iter < 1) return fail(CHK_EINVAL, "max_iter must be >= 1");
+  const int n = grid->n;
+  Workspace w = carve(workspace, n, B, opts->max_iter);
+  if (!workspace || workspace_bytes < w.bytes) return fail(CHK_EINVAL, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PlanDev pl = plan_dev(plan);
+  SolveCtl ctl{w.st, w.part, w.hist, maxblk_of(n), opts->max_iter, opts->tol,
+               opts->precond_residual_stopping ? 1 : 0};
+  RState* hst_all = g_pinned.get((size_t)2 * B);
+  RState* hst = hst_all;
+  if (!hst_all) return fail(CHK_ECUDA, "cudaMallocHost failed");
+  CHK_CUDA(cudaMemsetAsync(w.st, 0, sizeof(RState) * B, s));
+  CHK_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(double) * (size_t)opts->max_iter * B, s));
+
+  cudaEvent_t ev[2];
+  CHK_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CHK_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  auto run = [&]() -> int {
+    int rc2 = CHK_OK;
+    CHK_DISPATCH(n, {
+      // initialisation: r = f (projected), u = 0, z = P r, p = z  (solver.py:131-156)
+      if ((rc2 = O::rhs_stats(s, B, f, ctl))) return rc2;
+      if ((rc2 = O::fwd(FWD_INIT, s, B, g, beta, f, u, w.r, w.S, pl, ctl, 0))) return rc2;
+      if ((rc2 = O::mid(MID_PCG, s, B, w.S, pl, ctl, 0))) return rc2;
+      if ((rc2 = O::inv(INV_PCG, s, B, w.S, w.p, pl, ctl, 0))) return rc2;
+      // iterations, polled every `chunk` with one chunk of look-ahead
+      const int chunk = (n >= 128) ? 2 : 8;
+      int polled_upto = 0;
+      bool pending = false;
+      int ev_i = 0;
+      for (int it = 1; it <= opts->max_iter; ++it) {
+        if ((rc2 = O::dot(s, B, g, beta, w.p, ctl, it))) return rc2;
+        if ((rc2 = O::fwd(FWD_ITER, s, B, g, beta, w.p, u, w.r, w.S, pl, ctl, it))) return rc2;
+        if ((rc2 = O::mid(MID_PCG, s, B, w.S, pl, ctl, it))) return rc2;
+        if ((rc2 = O::inv(INV_PCG, s, B, w.S, w.p, pl, ctl, it))) return rc2;
+        if (it % chunk == 0 || it == opts->max_iter) {
+          if (pending) {
+            CHK_CUDA(cudaEventSynchronize(ev[ev_i ^ 1]));
+            const RState* prev = hst_all + (size_t)(ev_i ^ 1) * B;
+            bool any = false;
+            for (int b = 0; b < B; ++b) any |= (prev[b].status == ST_ACTIVE);
+            if (!any) break;
+          }
+          CHK_CUDA(cudaMemcpyAsync(hst_all + (size_t)ev_i * B, w.st, sizeof(RState) * B,
+                                   cudaMemcpyDeviceToHost, s));
+          CHK_CUDA(cudaEventRecord(ev[ev_i], s));
+          ev_i ^= 1;
+          pending = true;
+          polled_upto = it;
+        }
+      }
+      (void)polled_upto;
+      if ((rc2 = O::mean_u(s, B, u, ctl))) return rc2;
+    });
+    {
+      const size_t nb = (size_t)n * n * n;
+      sub_mean_kernel<<<1184, 256, 0, s>>>(u, w.st, nb, B);
+      CHK_LAUNCHED();
+    }
+    return rc2;
+  };
+  rc = run();
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  if (rc) return rc;
+  CHK_CUDA(cudaMemcpyAsync(hst, w.st, sizeof(RState) * B, cudaMemcpyDeviceToHost, s));
+  if (history)
+    CHK_CUDA(cudaMemcpyAsync(history, w.hist, sizeof(double) * (size_t)opts->max_iter * B,
+                             cudaMemcpyDeviceToHost, s));
+  CHK_CUDA(cudaStreamSynchronize(s));
+  g_prof.collect();
+  for (int b = 0; b < B; ++b) {
+    int stt = hst[b].status;
+    if (stt == ST_ACTIVE) stt = ST_NOT_CONVERGED;  // defensive; max_iter always decides
+    if (status) status[b] = stt;
+    if (iterations) iterations[b] = hst[b].iters;
+    if (final_rel) final_rel[b] = hst[b].final_rel;
+    if (rhs_projected) rhs_projected[b] = hst[b].rhs_projected;
+  }
+  return CHK_OK;
+}
+
+}  // extern "C"

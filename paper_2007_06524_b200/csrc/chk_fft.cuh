@@ -1,0 +1,178 @@
+// chk_fft.cuh -- fp64 complex helpers and shared-memory FFT stages (sm_100a).
+//
+// All transforms are in-place mixed-radix (8, then 4/2) on pencils that live in
+// shared memory.  The forward transform is decimation-in-frequency and leaves
+// frequency k at the digit-reversed position pos(k); the inverse is the exact
+// reverse (decimation-in-time, conjugate twiddles) and consumes that order, so a
+// forward -> pointwise scale -> inverse chain never permutes data.  Twiddles come
+// from one table w[k] = exp(-2 pi i k / ntab), k < ntab, computed on the host in
+// fp64 (the reference uses numpy's pocketfft, lowrank.py:190-192).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace chk {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+__device__ __forceinline__ double2 cmul_mi(double2 a) {
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft2(double2& a, double2& b) {
+  double2 t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3) {
+  double2 s0 = cadd(x0, x2), d0 = csub(x0, x2);
+  double2 s1 = cadd(x1, x3), d1 = cmul_mi<INV>(csub(x1, x3));
+  x0 = cadd(s0, s1);
+  x2 = csub(s0, s1);
+  x1 = cadd(d0, d1);
+  x3 = csub(d0, d1);
+}
+
+// y_m = sum_t v_t w8^{tm}, natural order in and out.
+template <bool INV>
+__device__ __forceinline__ void dft8(double2 (&v)[8]) {
+  constexpr double c = 0.70710678118654752440084436210485;
+  double2 a0 = v[0], a1 = v[2], a2 = v[4], a3 = v[6];
+  double2 b0 = v[1], b1 = v[3], b2 = v[5], b3 = v[7];
+  dft4<INV>(a0, a1, a2, a3);
+  dft4<INV>(b0, b1, b2, b3);
+  // b_m *= w8^m
+  if (!INV) {
+    b1 = make_double2(c * (b1.x + b1.y), c * (b1.y - b1.x));
+    b2 = make_double2(b2.y, -b2.x);
+    b3 = make_double2(c * (b3.y - b3.x), -c * (b3.x + b3.y));
+  } else {
+    b1 = make_double2(c * (b1.x - b1.y), c * (b1.y + b1.x));
+    b2 = make_double2(-b2.y, b2.x);
+    b3 = make_double2(-c * (b3.x + b3.y), c * (b3.x - b3.y));
+  }
+  v[0] = cadd(a0, b0); v[4] = csub(a0, b0);
+  v[1] = cadd(a1, b1); v[5] = csub(a1, b1);
+  v[2] = cadd(a2, b2); v[6] = csub(a2, b2);
+  v[3] = cadd(a3, b3); v[7] = csub(a3, b3);
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dftR(double2 (&v)[R]) {
+  if constexpr (R == 8) {
+    dft8<INV>(v);
+  } else if constexpr (R == 4) {
+    dft4<INV>(v[0], v[1], v[2], v[3]);
+  } else {
+    dft2<INV>(v[0], v[1]);
+  }
+}
+
+template <int M>
+struct Radix {
+  static constexpr int value = (M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2);
+};
+
+// One in-place stage at sub-length M of a length-N transform over `npencil`
+// pencils; element e of pencil p is at buf[addr(p, e)].  Consecutive threads
+// take consecutive pencils (callers lay pencils out bank-conflict free).
+template <int N, int M, bool INV, class Addr>
+__device__ __forceinline__ void fft_stage(double2* buf, int npencil, const Addr& addr,
+                                          const double2* __restrict__ tw, int twstride) {
+  constexpr int R = Radix<M>::value;
+  constexpr int S = M / R;
+  constexpr int NBF = N / R;
+  const int total = npencil * NBF;
+  for (int w = threadIdx.x; w < total; w += blockDim.x) {
+    const int p = w % npencil;
+    const int bf = w / npencil;
+    const int blk = bf / S, j = bf - (bf / S) * S;
+    const int base = blk * M + j;
+    double2 v[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) v[t] = buf[addr(p, base + t * S)];
+    if (!INV) {
+      dftR<R, false>(v);
+      if (S > 1) {
+#pragma unroll
+        for (int m = 1; m < R; ++m) v[m] = cmul(v[m], __ldg(tw + (j * m * (N / M)) * twstride));
+      }
+    } else {
+      if (S > 1) {
+#pragma unroll
+        for (int m = 1; m < R; ++m) v[m] = cmulc(v[m], __ldg(tw + (j * m * (N / M)) * twstride));
+      }
+      dftR<R, true>(v);
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) buf[addr(p, base + t * S)] = v[t];
+  }
+}
+
+template <int N, int M, bool INV>
+struct FftRec {
+  template <class Addr>
+  __device__ __forceinline__ static void run(double2* buf, int npencil, const Addr& addr,
+                                             const double2* __restrict__ tw, int twstride) {
+    constexpr int R = Radix<M>::value;
+    if constexpr (!INV) {
+      fft_stage<N, M, false>(buf, npencil, addr, tw, twstride);
+      __syncthreads();
+      if constexpr (M / R > 1) FftRec<N, M / R, false>::run(buf, npencil, addr, tw, twstride);
+    } else {
+      if constexpr (M / R > 1) FftRec<N, M / R, true>::run(buf, npencil, addr, tw, twstride);
+      fft_stage<N, M, true>(buf, npencil, addr, tw, twstride);
+      __syncthreads();
+    }
+  }
+};
+
+// Full length-N transform; the caller must __syncthreads() before (data in
+// smem); returns after a __syncthreads().  Forward: natural -> digit-reversed.
+// Inverse (unnormalised): digit-reversed -> natural, result scaled by N.
+template <int N, bool INV, class Addr>
+__device__ __forceinline__ void fft_smem(double2* buf, int npencil, const Addr& addr,
+                                         const double2* __restrict__ tw, int ntab) {
+  if constexpr (N > 1) FftRec<N, N, INV>::run(buf, npencil, addr, tw, ntab / N);
+}
+
+// ----------------------------------------------------------------------------
+// reductions (deterministic: fixed shuffle tree, fixed warp order)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block sum; result valid in every thread.  `scratch` >= 32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double t = (threadIdx.x < nw) ? scratch[threadIdx.x] : 0.0;
+  if (wid == 0) t = warp_sum(t);
+  if (threadIdx.x == 0) scratch[0] = t;
+  __syncthreads();
+  double r = scratch[0];
+  __syncthreads();
+  return r;
+}
+
+}  // namespace chk

@@ -1,0 +1,723 @@
+// chk_kernels.cuh -- sm_100a kernels of the batched PCG hot path.
+//
+// Per PCG iteration k >= 1 (pcg_solve loop, solver.py:161-185) four kernels run
+// over all B realizations of the batch (CTA = one (realization, x0-plane,
+// x1-group) slab or one spectral column tile):
+//
+//   stencil_dot   pq  = <p, A p>                                  (solver.py:162-165)
+//   fwd_plane     u += a p ; r -= a A p ; ||r||^2 ; stop test ;    (solver.py:166-177)
+//                 then R2C along x2 + C2C along the x1 group of r
+//   mid_column    C2C along x1 (group combine) and x0, scale by the  (lowrank.py:189-192)
+//                 rank-R canonical diagonal evaluated on the fly,
+//                 <r, z> by Parseval, inverse along x0 / x1 group
+//   inv_plane     inverse C2C x1 group + C2R x2 -> z ; p = z + b p  (solver.py:179-185)
+//
+// The stiffness never exists as a matrix: A is the 7-point edge-weighted
+// stencil of tests/oracles.py:35-82 with edge conductivities built from the
+// compact L^3 cell array on the fly.  The diagonal D[i,j,l] = sum_k U0[k,i]
+// U1[k,j] U2[k,l] is never materialised.  Reductions are deterministic: every
+// CTA writes a partial, the last CTA of the realization (atomic ticket) sums
+// them in a fixed order and takes the scalar decisions (alpha, beta, stop).
+#pragma once
+#include "chk_fft.cuh"
+
+namespace chk {
+
+enum : int { ST_CONVERGED = 0, ST_NOT_CONVERGED = 1, ST_BREAKDOWN = 2, ST_ACTIVE = 3 };
+enum : int { KIND_FOURIER = 0, KIND_LKR = 1, KIND_REGULARIZED = 2 };
+
+// Per-realization solver state (device).
+struct RState {
+  int status;
+  int iters;
+  int rhs_projected;
+  int pad0;
+  double normf;      // ||f|| after the optional mean projection (solver.py:132,142)
+  double norm_pf;    // sqrt|r0.z0| (solver.py:156)
+  double mean_f;     // mean removed from f when projected
+  double rz[2];      // r.z of the last two iterations (parity-indexed)
+  double pq;         // p.Ap of the current iteration
+  double beta;       // rz_k / rz_{k-1}
+  double final_rel;  // last relative residual
+  double mean_u;     // final projection (solver.py:169)
+  unsigned cnt;      // last-block ticket
+  unsigned pad1;
+};
+
+struct Geo {
+  int n;
+  int L;
+  int sh;    // log2 n0
+  int mask;  // n0 - 1
+  int k;     // sub-cell width
+  int off;   // sub-cell offset
+  double lam;
+};
+
+struct SolveCtl {
+  RState* st;        // [B]
+  double* part;      // [B][maxblk][2]
+  double* hist;      // [B][max_iter] or null
+  int maxblk;
+  int max_iter;
+  double tol;
+  int prs;           // precond_residual_stopping
+};
+
+struct PlanDev {
+  const double2* tw;  // [n] exp(-2 pi i k / n)
+  const double* U;    // [3][r1][n] (LKR)
+  const double* lam;  // [n] eigenvalues (FOURIER / REGULARIZED)
+  int r1;
+  int kind;
+  double delta;
+};
+
+// ----------------------------------------------------------------------------
+// digit-reversed position <-> frequency for the radix sequence of fft_smem
+// ----------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ int dig_pos(int k) {
+  int p = 0;
+  int M = N;
+#pragma unroll
+  for (int s = 0; s < 12; ++s) {
+    if (M <= 1) break;
+    const int R = (M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2);
+    const int m = k % R;
+    k /= R;
+    p += m * (M / R);
+    M /= R;
+  }
+  return p;
+}
+template <int N>
+__device__ __forceinline__ int dig_freq(int p) {
+  int k = 0, mul = 1;
+  int M = N;
+#pragma unroll
+  for (int s = 0; s < 12; ++s) {
+    if (M <= 1) break;
+    const int R = (M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2);
+    const int Mn = M / R;
+    const int m = p / Mn;
+    p -= m * Mn;
+    k += m * mul;
+    mul *= R;
+    M = Mn;
+  }
+  return k;
+}
+
+// ----------------------------------------------------------------------------
+// last-block reduction of two scalars per realization
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ bool reduce2_last(double v0, double v1, double* part, unsigned* cnt,
+                                             int blk, int nblk, double* scratch, double& t0,
+                                             double& t1) {
+  __shared__ int s_last;
+  v0 = block_sum(v0, scratch);
+  v1 = block_sum(v1, scratch);
+  if (threadIdx.x == 0) {
+    part[2 * blk] = v0;
+    part[2 * blk + 1] = v1;
+    __threadfence();
+    const unsigned prev = atomicAdd(cnt, 1u);
+    s_last = (prev == (unsigned)(nblk - 1));
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  double a = 0.0, c = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    a += __ldcg(part + 2 * i);
+    c += __ldcg(part + 2 * i + 1);
+  }
+  t0 = block_sum(a, scratch);
+  t1 = block_sum(c, scratch);
+  if (threadIdx.x == 0) *cnt = 0u;
+  return true;
+}
+
+// ----------------------------------------------------------------------------
+// stiffness: 7-point stencil with on-the-fly edge conductivities
+// ----------------------------------------------------------------------------
+// F of h-cell (j0, j1, j2): beta(cell) if the h-cell lies inside the sub-cell
+// on every axis (lattice.py:314-317,326-332), else 0.
+__device__ __forceinline__ double fcell(const double* __restrict__ beta, const Geo& g, int j0,
+                                        int j1, int j2) {
+  const bool in = ((unsigned)((j0 & g.mask) - g.off) < (unsigned)g.k) &&
+                  ((unsigned)((j1 & g.mask) - g.off) < (unsigned)g.k) &&
+                  ((unsigned)((j2 & g.mask) - g.off) < (unsigned)g.k);
+  return in ? __ldg(beta + ((j0 >> g.sh) * g.L + (j1 >> g.sh)) * g.L + (j2 >> g.sh)) : 0.0;
+}
+
+// (A p)_x for node x of one realization (p, beta already offset).
+//   g_a(x) = lam + 1/4 sum_{delta} F[h-cell x_a, transverse x_b - delta_b]
+//   (A p)_x = sum_a g_a(x)(p_x - p_{x+e_a}) + g_a(x-e_a)(p_x - p_{x-e_a})
+// (tests/oracles.py:52-75; transverse delta order of the reference loop).
+__device__ __forceinline__ double stencil_node(const double* __restrict__ p,
+                                               const double* __restrict__ beta, const Geo& g,
+                                               int x0, int x1, int x2, double& pc) {
+  const int n = g.n, nm = n - 1;
+  const int a0 = (x0 - 1) & nm, a1 = (x1 - 1) & nm, a2 = (x2 - 1) & nm;
+  const int p0 = (x0 + 1) & nm, p1 = (x1 + 1) & nm, p2 = (x2 + 1) & nm;
+  // F[a][b][c], a: {x0-1, x0}, b: {x1-1, x1}, c: {x2-1, x2}
+  const double f000 = fcell(beta, g, a0, a1, a2), f001 = fcell(beta, g, a0, a1, x2);
+  const double f010 = fcell(beta, g, a0, x1, a2), f011 = fcell(beta, g, a0, x1, x2);
+  const double f100 = fcell(beta, g, x0, a1, a2), f101 = fcell(beta, g, x0, a1, x2);
+  const double f110 = fcell(beta, g, x0, x1, a2), f111 = fcell(beta, g, x0, x1, x2);
+  const double lam = g.lam;
+  // axis 0 edge x->x+e0: h-cell j0 = x0, delta over (x1, x2)
+  const double g0p = lam + (((f111 + f110) + f101) + f100) * 0.25;
+  const double g0m = lam + (((f011 + f010) + f001) + f000) * 0.25;
+  // axis 1 edge: j1 = x1, delta over (x0, x2)
+  const double g1p = lam + (((f111 + f110) + f011) + f010) * 0.25;
+  const double g1m = lam + (((f101 + f100) + f001) + f000) * 0.25;
+  // axis 2 edge: j2 = x2, delta over (x0, x1)
+  const double g2p = lam + (((f111 + f101) + f011) + f001) * 0.25;
+  const double g2m = lam + (((f110 + f100) + f010) + f000) * 0.25;
+  const size_t nn = (size_t)n * n;
+  const size_t row = (size_t)x0 * nn + (size_t)x1 * n;
+  pc = __ldg(p + row + x2);
+  const double q0 = g0p * (pc - __ldg(p + (size_t)p0 * nn + (size_t)x1 * n + x2)) +
+                    g0m * (pc - __ldg(p + (size_t)a0 * nn + (size_t)x1 * n + x2));
+  const double q1 = g1p * (pc - __ldg(p + (size_t)x0 * nn + (size_t)p1 * n + x2)) +
+                    g1m * (pc - __ldg(p + (size_t)x0 * nn + (size_t)a1 * n + x2));
+  const double q2 = g2p * (pc - __ldg(p + row + p2)) + g2m * (pc - __ldg(p + row + a2));
+  return (q0 + q1) + q2;
+}
+
+// Standalone matvec y = A x (+ optional <x, y>), CTA per (realization, x0, group).
+template <int N, int G>
+__global__ void __launch_bounds__(256) stencil_apply_kernel(Geo g, const double* __restrict__ beta,
+                                                            const double* __restrict__ x,
+                                                            double* __restrict__ y, double* xy,
+                                                            double* part, unsigned* cnt) {
+  constexpr int NR = N / G;
+  __shared__ double scratch[32];
+  const int b = blockIdx.x / (N * G);
+  const int rem = blockIdx.x - b * (N * G);
+  const int x0 = rem / G, gg = rem - (rem / G) * G;
+  const size_t nb = (size_t)N * N * N;
+  const double* xb = x + b * nb;
+  const double* bb = beta + (size_t)b * g.L * g.L * g.L;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
+    const int t = i / N, x2 = i - (i / N) * N;
+    const int x1 = gg + G * t;
+    double pc;
+    const double q = stencil_node(xb, bb, g, x0, x1, x2, pc);
+    y[b * nb + ((size_t)x0 * N + x1) * N + x2] = q;
+    acc += pc * q;
+  }
+  if (xy != nullptr) {
+    double t0, t1;
+    if (reduce2_last(acc, 0.0, part + (size_t)b * 2 * N * G, cnt + b, rem, N * G, scratch, t0, t1)) {
+      if (threadIdx.x == 0) xy[b] = t0;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// corrector right-hand side (homogenize.py:75-89 with lattice.py:335-345)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double nodal_coef(const double* __restrict__ beta, const Geo& g, int x0,
+                                             int x1, int x2) {
+  // c[x] = 1/8 sum_{delta in {0,1}^3} F[x - delta]: lattice.py:342-345 applies
+  // 0.5*(v + roll(v,1)) axis by axis; replicate that order.
+  const int nm = g.n - 1;
+  const int a0 = (x0 - 1) & nm, a1 = (x1 - 1) & nm, a2 = (x2 - 1) & nm;
+  // axis 0 first
+  auto c0 = [&](int j1, int j2) { return 0.5 * (fcell(beta, g, x0, j1, j2) + fcell(beta, g, a0, j1, j2)); };
+  auto c1 = [&](int j2) { return 0.5 * (c0(x1, j2) + c0(a1, j2)); };
+  return 0.5 * (c1(x2) + c1(a2));
+}
+
+template <int N>
+__global__ void __launch_bounds__(256) corrector_rhs_kernel(Geo g, const double* __restrict__ beta,
+                                                            double* __restrict__ f, int axis,
+                                                            double scale) {
+  const size_t nb = (size_t)N * N * N;
+  const int b = blockIdx.y;
+  const double* bb = beta + (size_t)b * g.L * g.L * g.L;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int x2 = (int)(i % N), x1 = (int)((i / N) % N), x0 = (int)(i / ((size_t)N * N));
+    int xp[3] = {x0, x1, x2}, xm[3] = {x0, x1, x2};
+    xp[axis] = (xp[axis] + 1) & (N - 1);
+    xm[axis] = (xm[axis] - 1) & (N - 1);
+    const double cp = nodal_coef(bb, g, xp[0], xp[1], xp[2]);
+    const double cm = nodal_coef(bb, g, xm[0], xm[1], xm[2]);
+    f[b * nb + i] = scale * (0.5 * (cp - cm));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// shared-memory addressing of the plane and column tiles
+// ----------------------------------------------------------------------------
+struct RowAddr {  // pencil = row t (stride HP), element along k2
+  int hp;
+  __device__ __forceinline__ int operator()(int p, int e) const { return p * hp + e; }
+};
+struct ColAddr {  // pencil = k2 column, element along rows
+  int hp;
+  __device__ __forceinline__ int operator()(int p, int e) const { return e * hp + p; }
+};
+struct X0Addr {  // middle tile: pencil = slot s, element along x0 rows (stride rs)
+  int rs;
+  __device__ __forceinline__ int operator()(int p, int e) const { return e * rs + p; }
+};
+template <int W>
+struct GAddr {  // middle tile: pencil = (x0, w), element = group slot g
+  int rs;
+  __device__ __forceinline__ int operator()(int p, int e) const {
+    return (p / W) * rs + e * W + (p % W);
+  }
+};
+
+// Half-length real FFT post-processing, in place at digit-reversed positions of
+// each row (length N/2 complex + slot N/2 for the Nyquist term).
+template <int N>
+__device__ __forceinline__ void r2c_post(double2* buf, int nrows, int hp,
+                                         const double2* __restrict__ tw) {
+  constexpr int N2 = N / 2;
+  constexpr int NP = N2 / 2 + 1;
+  for (int i = threadIdx.x; i < nrows * NP; i += blockDim.x) {
+    const int t = i % nrows, k = i / nrows;
+    double2* row = buf + t * hp;
+    const int kc = (N2 - k) & (N2 - 1);
+    const int q = dig_pos<N2>(k), qc = dig_pos<N2>(kc);
+    const double2 zk = row[q];
+    const double2 zc = cconj(row[qc]);
+    const double2 s = cadd(zk, zc), d = csub(zk, zc);
+    const double2 E = make_double2(0.5 * s.x, 0.5 * s.y);
+    const double2 O = make_double2(0.5 * d.y, -0.5 * d.x);  // -i d / 2
+    if (k == 0) {
+      row[q] = make_double2(E.x + O.x, 0.0);
+      row[N2] = make_double2(E.x - O.x, 0.0);
+    } else {
+      const double2 a = cadd(E, cmul(__ldg(tw + k), O));
+      const double2 c = cadd(cconj(E), cmul(__ldg(tw + (N2 - k)), cconj(O)));
+      row[q] = a;
+      row[qc] = c;
+    }
+  }
+}
+
+// Inverse of r2c_post: X (permuted + Nyquist slot) -> Z at digit-reversed positions.
+template <int N>
+__device__ __forceinline__ void c2r_pre(double2* buf, int nrows, int hp,
+                                        const double2* __restrict__ tw) {
+  constexpr int N2 = N / 2;
+  constexpr int NP = N2 / 2 + 1;
+  for (int i = threadIdx.x; i < nrows * NP; i += blockDim.x) {
+    const int t = i % nrows, k = i / nrows;
+    double2* row = buf + t * hp;
+    const int kc = (N2 - k) & (N2 - 1);
+    const int q = dig_pos<N2>(k), qc = dig_pos<N2>(kc);
+    const double2 xk = row[q];
+    const double2 xc = (k == 0) ? row[N2] : row[qc];
+    {
+      const double2 s = cadd(xk, cconj(xc));
+      const double2 d = cmulc(csub(xk, cconj(xc)), __ldg(tw + k));
+      // Z = E + i O with E = s/2, O = d/2
+      row[q] = make_double2(0.5 * (s.x - d.y), 0.5 * (s.y + d.x));
+    }
+    if (k != 0 && kc != k) {
+      const double2 s = cadd(xc, cconj(xk));
+      const double2 d = cmulc(csub(xc, cconj(xk)), __ldg(tw + kc));
+      row[qc] = make_double2(0.5 * (s.x - d.y), 0.5 * (s.y + d.x));
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// kernel 1: pq = <p, A p>  (solver.py:162-165)
+// ----------------------------------------------------------------------------
+template <int N, int G>
+__global__ void __launch_bounds__(256) stencil_dot_kernel(Geo g, const double* __restrict__ beta,
+                                                          const double* __restrict__ p,
+                                                          SolveCtl ctl, int it) {
+  constexpr int NR = N / G;
+  __shared__ double scratch[32];
+  const int b = blockIdx.x / (N * G);
+  const int rem = blockIdx.x - b * (N * G);
+  RState* st = ctl.st + b;
+  if (st->status != ST_ACTIVE) return;
+  const int x0 = rem / G, gg = rem - (rem / G) * G;
+  const size_t nb = (size_t)N * N * N;
+  const double* pb = p + b * nb;
+  const double* bb = beta + (size_t)b * g.L * g.L * g.L;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
+    const int t = i / N, x2 = i - (i / N) * N;
+    double pc;
+    const double q = stencil_node(pb, bb, g, x0, gg + G * t, x2, pc);
+    acc += pc * q;
+  }
+  double t0, t1;
+  if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G, scratch,
+                   t0, t1)) {
+    if (threadIdx.x == 0) {
+      if (!(t0 > 0.0) || !isfinite(t0)) {  // solver.py:164-165
+        st->status = ST_BREAKDOWN;
+        st->iters = it;
+      }
+      st->pq = t0;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// kernel 2: vector update + forward plane transform
+// ----------------------------------------------------------------------------
+enum : int { FWD_APPLY = 0, FWD_INIT = 1, FWD_ITER = 2 };
+
+template <int N, int G, int MODE>
+__global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __restrict__ beta,
+                                                        const double* __restrict__ src,  // x (APPLY) / f (INIT) / p (ITER)
+                                                        double* __restrict__ u, double* __restrict__ r,
+                                                        double2* __restrict__ S, PlanDev pl,
+                                                        SolveCtl ctl, int it) {
+  constexpr int NR = N / G;
+  constexpr int N2 = N / 2;
+  constexpr int H = N2 + 1;
+  constexpr int HP = H;
+  extern __shared__ double2 buf[];
+  __shared__ double scratch[32];
+  const int b = blockIdx.x / (N * G);
+  const int rem = blockIdx.x - b * (N * G);
+  const int x0 = rem / G, gg = rem - (rem / G) * G;
+  const size_t nb = (size_t)N * N * N;
+  double* sm = reinterpret_cast<double*>(buf);
+  RState* st = (MODE == FWD_APPLY) ? nullptr : ctl.st + b;
+
+  if (MODE == FWD_APPLY) {
+    for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
+      const int t = i / N, x2 = i - (i / N) * N;
+      sm[t * 2 * HP + x2] = __ldg(src + b * nb + ((size_t)x0 * N + gg + G * t) * N + x2);
+    }
+  } else if (MODE == FWD_INIT) {
+    const int status = st->status;
+    const double shift = st->rhs_projected ? st->mean_f : 0.0;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
+      const int t = i / N, x2 = i - (i / N) * N;
+      const size_t idx = b * nb + ((size_t)x0 * N + gg + G * t) * N + x2;
+      u[idx] = 0.0;
+      const double rv = __ldg(src + idx) - shift;
+      r[idx] = rv;
+      sm[t * 2 * HP + x2] = rv;
+      acc += rv * rv;
+    }
+    if (status != ST_ACTIVE) return;
+    double t0, t1;
+    if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G,
+                     scratch, t0, t1)) {
+      if (threadIdx.x == 0) {
+        st->normf = sqrt(t0);
+        if (!(t0 > 0.0)) {  // projected RHS vanished (solver.py:144-148)
+          st->status = ST_CONVERGED;
+          st->iters = 0;
+          st->final_rel = 0.0;
+        }
+      }
+    }
+  } else {  // FWD_ITER
+    if (st->status != ST_ACTIVE) return;
+    const double alpha = st->rz[(it - 1) & 1] / st->pq;  // solver.py:166
+    const double* pb = src + b * nb;
+    const double* bb = beta + (size_t)b * g.L * g.L * g.L;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
+      const int t = i / N, x2 = i - (i / N) * N;
+      const int x1 = gg + G * t;
+      const size_t idx = b * nb + ((size_t)x0 * N + x1) * N + x2;
+      double pc;
+      const double q = stencil_node(pb, bb, g, x0, x1, x2, pc);
+      u[idx] = u[idx] + alpha * pc;           // solver.py:167
+      const double rv = r[idx] - alpha * q;   // solver.py:168
+      r[idx] = rv;
+      sm[t * 2 * HP + x2] = rv;
+      acc += rv * rv;
+    }
+    double t0, t1;
+    if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G,
+                     scratch, t0, t1)) {
+      if (threadIdx.x == 0) {
+        const double rel = sqrt(t0) / st->normf;  // solver.py:171
+        if (ctl.hist) ctl.hist[(size_t)b * ctl.max_iter + (it - 1)] = rel;
+        st->final_rel = rel;
+        if (!isfinite(rel)) {  // solver.py:172-173
+          st->status = ST_BREAKDOWN;
+          st->iters = it;
+        } else if (!ctl.prs && rel <= ctl.tol) {  // solver.py:175-177
+          st->status = ST_CONVERGED;
+          st->iters = it;
+        } else if (!ctl.prs && it >= ctl.max_iter) {
+          st->status = ST_NOT_CONVERGED;
+          st->iters = it;
+        }
+      }
+    }
+    // other CTAs of this realization still have to transform their r slab only
+    // if the iteration continues; the decision is known only to the last CTA,
+    // so every CTA transforms (the middle kernel skips converged realizations).
+  }
+  __syncthreads();
+  // R2C along x2: rows of N reals viewed as N/2 complex (z_m = x_2m + i x_2m+1)
+  fft_smem<N2, false>(buf, NR, RowAddr{HP}, pl.tw, N);
+  r2c_post<N>(buf, NR, HP, pl.tw);
+  __syncthreads();
+  // C2C along the x1 group (length NR)
+  fft_smem<NR, false>(buf, H, ColAddr{HP}, pl.tw, N);
+  double2* dst = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
+  for (int i = threadIdx.x; i < NR * H; i += blockDim.x) dst[i] = buf[i];
+}
+
+// ----------------------------------------------------------------------------
+// kernel 3: spectral column pass (x1 group combine + x0), diagonal scaling
+// ----------------------------------------------------------------------------
+enum : int { MID_APPLY = 0, MID_PCG = 1 };
+
+template <int N, int G, int W, int MODE>
+__global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S, PlanDev pl,
+                                                         SolveCtl ctl, int it) {
+  constexpr int NR = N / G;
+  constexpr int N2 = N / 2;
+  constexpr int H = N2 + 1;
+  constexpr int TILES = NR * H / W;
+  constexpr int GW = G * W;
+  constexpr int RS = GW + 1;
+  extern __shared__ double2 buf[];
+  __shared__ double scratch[32];
+  __shared__ int s_k1[GW], s_k2[GW];
+  const int b = blockIdx.x / TILES;
+  const int tile = blockIdx.x - b * TILES;
+  const int c0 = tile * W;
+  RState* st = (MODE == MID_PCG) ? ctl.st + b : nullptr;
+  if (MODE == MID_PCG && st->status != ST_ACTIVE) return;
+  double* coef = reinterpret_cast<double*>(buf + N * RS);  // [r1][GW] (LKR)
+
+  // column bookkeeping: slot s = m*W + w  <->  (k1, k2)
+  for (int s = threadIdx.x; s < GW; s += blockDim.x) {
+    const int m = dig_freq<G>(s / W), w = s % W;
+    const int c = c0 + w;
+    const int q1 = c / H, q2 = c - (c / H) * H;
+    const int kp = dig_freq<NR>(q1);
+    s_k1[s] = kp + m * NR;
+    s_k2[s] = (q2 == N2) ? N2 : dig_freq<N2>(q2);
+  }
+  // load the tile; apply the group-combine twiddle w_n^(g k') on the fly
+  const double2* src = S + (size_t)b * N * G * (NR * H);
+  for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
+    const int w = i % W, gq = (i / W) % G, x0 = i / GW;
+    double2 v = src[((size_t)x0 * G + gq) * (NR * H) + c0 + w];
+    if (G > 1) {
+      const int c = c0 + w;
+      const int kp = dig_freq<NR>(c / H);
+      v = cmul(v, __ldg(pl.tw + gq * kp));
+    }
+    buf[x0 * RS + gq * W + w] = v;
+  }
+  __syncthreads();
+  if (pl.kind == KIND_LKR) {
+    const double* U1 = pl.U + (size_t)pl.r1 * N;
+    const double* U2 = pl.U + (size_t)2 * pl.r1 * N;
+    for (int i = threadIdx.x; i < pl.r1 * GW; i += blockDim.x) {
+      const int s = i % GW, rr = i / GW;
+      coef[rr * GW + s] = __ldg(U1 + rr * N + s_k1[s]) * __ldg(U2 + rr * N + s_k2[s]);
+    }
+  }
+  if (G > 1) fft_smem<G, false>(buf, N * W, GAddr<W>{RS}, pl.tw, N);
+  fft_smem<N, false>(buf, GW, X0Addr{RS}, pl.tw, N);
+
+  // diagonal scaling (+ Parseval r.z for the PCG)
+  const double scale = 2.0 / ((double)N * N * N);
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
+    const int s = i % GW, pos0 = i / GW;
+    const int k0 = dig_freq<N>(pos0);
+    const int k1 = s_k1[s], k2 = s_k2[s];
+    double D;
+    if (pl.kind == KIND_LKR) {
+      D = 0.0;
+      const double* U0 = pl.U + k0;
+      for (int rr = 0; rr < pl.r1; ++rr) D = fma(__ldg(U0 + rr * N), coef[rr * GW + s], D);
+    } else {
+      const double gsum = (__ldg(pl.lam + k0) + __ldg(pl.lam + k1)) + __ldg(pl.lam + k2);
+      if (pl.kind == KIND_REGULARIZED && pl.delta > 0.0) {
+        D = 1.0 / (gsum + pl.delta);
+      } else {
+        D = (gsum > 0.0) ? 1.0 / gsum : 0.0;
+      }
+    }
+    double2 v = buf[pos0 * RS + s];
+    if (MODE == MID_PCG) {
+      if ((k0 | k1 | k2) == 0) {
+        D = 0.0;  // mean projection of z (solver.py:153,179)
+      }
+      const double wgt = (k2 == 0 || k2 == N2) ? 1.0 : 2.0;
+      acc = fma(wgt * D, v.x * v.x + v.y * v.y, acc);
+    }
+    buf[pos0 * RS + s] = cscale(v, D * scale);
+  }
+  __syncthreads();
+  fft_smem<N, true>(buf, GW, X0Addr{RS}, pl.tw, N);
+  if (G > 1) fft_smem<G, true>(buf, N * W, GAddr<W>{RS}, pl.tw, N);
+  double2* dst = S + (size_t)b * N * G * (NR * H);
+  for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
+    const int w = i % W, gq = (i / W) % G, x0 = i / GW;
+    double2 v = buf[x0 * RS + gq * W + w];
+    if (G > 1) {
+      const int c = c0 + w;
+      const int kp = dig_freq<NR>(c / H);
+      v = cmulc(v, __ldg(pl.tw + gq * kp));
+    }
+    dst[((size_t)x0 * G + gq) * (NR * H) + c0 + w] = v;
+  }
+  if (MODE == MID_PCG) {
+    double t0, t1;
+    if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
+                     scratch, t0, t1)) {
+      if (threadIdx.x == 0) {
+        const double rz = t0 / ((double)N * N * N);  // Parseval: r.z = (1/N^3) sum conj(R) D R
+        if (it == 0) {
+          st->rz[0] = rz;
+          st->norm_pf = sqrt(fabs(rz));  // solver.py:156
+          st->beta = 0.0;
+        } else {
+          st->beta = rz / st->rz[(it - 1) & 1];  // solver.py:184
+          st->rz[it & 1] = rz;
+          if (ctl.prs && sqrt(fabs(rz)) / st->norm_pf <= ctl.tol) {  // solver.py:181-183
+            st->status = ST_CONVERGED;
+            st->iters = it;
+          } else if (it >= ctl.max_iter) {
+            st->status = ST_NOT_CONVERGED;
+            st->iters = it;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// kernel 4: inverse plane transform + direction update
+// ----------------------------------------------------------------------------
+enum : int { INV_APPLY = 0, INV_PCG = 1 };
+
+template <int N, int G, int MODE>
+__global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restrict__ S,
+                                                        double* __restrict__ out, PlanDev pl,
+                                                        SolveCtl ctl, int it) {
+  constexpr int NR = N / G;
+  constexpr int N2 = N / 2;
+  constexpr int H = N2 + 1;
+  constexpr int HP = H;
+  extern __shared__ double2 buf[];
+  const int b = blockIdx.x / (N * G);
+  const int rem = blockIdx.x - b * (N * G);
+  const int x0 = rem / G, gg = rem - (rem / G) * G;
+  const size_t nb = (size_t)N * N * N;
+  double beta = 0.0;
+  if (MODE == INV_PCG) {
+    RState* st = ctl.st + b;
+    if (st->status != ST_ACTIVE) return;
+    beta = st->beta;
+  }
+  const double2* srcp = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
+  for (int i = threadIdx.x; i < NR * H; i += blockDim.x) buf[i] = srcp[i];
+  __syncthreads();
+  fft_smem<NR, true>(buf, H, ColAddr{HP}, pl.tw, N);
+  c2r_pre<N>(buf, NR, HP, pl.tw);
+  __syncthreads();
+  fft_smem<N2, true>(buf, NR, RowAddr{HP}, pl.tw, N);
+  const double* sm = reinterpret_cast<const double*>(buf);
+  for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
+    const int t = i / N, x2 = i - (i / N) * N;
+    const size_t idx = b * nb + ((size_t)x0 * N + gg + G * t) * N + x2;
+    const double z = sm[t * 2 * HP + x2];
+    if (MODE == INV_APPLY) {
+      out[idx] = z;
+    } else {
+      out[idx] = (it == 0) ? z : z + beta * out[idx];  // solver.py:154,184
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// init / finalize reductions
+// ----------------------------------------------------------------------------
+template <int N, int G>
+__global__ void __launch_bounds__(256) rhs_stats_kernel(const double* __restrict__ f, SolveCtl ctl) {
+  constexpr int NR = N / G;
+  __shared__ double scratch[32];
+  const int b = blockIdx.x / (N * G);
+  const int rem = blockIdx.x - b * (N * G);
+  const int x0 = rem / G, gg = rem - (rem / G) * G;
+  const size_t nb = (size_t)N * N * N;
+  RState* st = ctl.st + b;
+  double s = 0.0, s2 = 0.0;
+  for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
+    const int t = i / N, x2 = i - (i / N) * N;
+    const double v = __ldg(f + b * nb + ((size_t)x0 * N + gg + G * t) * N + x2);
+    s += v;
+    s2 += v * v;
+  }
+  double t0, t1;
+  if (reduce2_last(s, s2, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G, scratch,
+                   t0, t1)) {
+    if (threadIdx.x == 0) {
+      const double normf = sqrt(t1);
+      st->iters = 0;
+      st->final_rel = 0.0;
+      st->rz[0] = st->rz[1] = 0.0;
+      st->beta = 0.0;
+      st->mean_u = 0.0;
+      if (!(normf > 0.0)) {  // zero right-hand side (solver.py:131-136)
+        st->status = ST_CONVERGED;
+        st->rhs_projected = 0;
+        st->mean_f = 0.0;
+      } else {
+        st->status = ST_ACTIVE;
+        st->rhs_projected = fabs(t0) > 1e-10 * normf ? 1 : 0;  // solver.py:139
+        st->mean_f = t0 / (double)nb;
+      }
+    }
+  }
+}
+
+template <int N, int G>
+__global__ void __launch_bounds__(256) mean_u_kernel(const double* __restrict__ u, SolveCtl ctl) {
+  constexpr int NR = N / G;
+  __shared__ double scratch[32];
+  const int b = blockIdx.x / (N * G);
+  const int rem = blockIdx.x - b * (N * G);
+  const int x0 = rem / G, gg = rem - (rem / G) * G;
+  const size_t nb = (size_t)N * N * N;
+  RState* st = ctl.st + b;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
+    const int t = i / N, x2 = i - (i / N) * N;
+    s += u[b * nb + ((size_t)x0 * N + gg + G * t) * N + x2];
+  }
+  double t0, t1;
+  if (reduce2_last(s, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G, scratch,
+                   t0, t1)) {
+    if (threadIdx.x == 0) st->mean_u = t0 / (double)nb;
+  }
+}
+
+__global__ void __launch_bounds__(256) sub_mean_kernel(double* __restrict__ u, const RState* st,
+                                                       size_t nb, int B) {
+  const size_t total = nb * (size_t)B;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / nb);
+    u[i] -= st[b].mean_u;  // solver.py:169 (applied once: proj is linear and idempotent)
+  }
+}
+
+}  // namespace chk

@@ -1,0 +1,36 @@
+import functools
+import os
+import sys
+
+import numpy as np
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if REPO not in sys.path:
+    sys.path.insert(0, REPO)
+TESTS = os.path.dirname(os.path.abspath(__file__))
+if TESTS not in sys.path:
+    sys.path.insert(0, TESTS)
+
+GOLDEN_DIR = os.path.join(TESTS, "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+
+
+@functools.lru_cache(maxsize=1)
+def golden_small():
+    return np.load(os.path.join(GOLDEN_DIR, "small.npz"))
+
+
+def golden_configs(cfg_id):
+    """All committed per-realization records of a BASELINE config."""
+    import glob
+    import json
+
+    recs = []
+    for path in sorted(glob.glob(os.path.join(GOLDEN_DIR, f"config{cfg_id}_*.json"))):
+        recs.extend(json.load(open(path))["records"])
+    recs.sort(key=lambda r: r["m"])
+    return recs

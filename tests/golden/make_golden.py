@@ -1,0 +1,241 @@
+"""Generate golden fixtures from the REFERENCE package (build container only).
+
+Imports the read-only reference ``checkerhom`` from /root/reference/pkg/src and
+records its outputs for the hot path.  The fixtures pin both the CPU oracle
+(oracle/checkerhom_oracle.py) and the CUDA path.  Run:
+
+    python tests/golden/make_golden.py small            # -> tests/golden/small.npz
+    python tests/golden/make_golden.py config 3 0 16    # -> tests/golden/config3_0_16.json
+
+Large arrays are never committed: for configs 2-5 we keep iteration counts,
+the full residual history, ||u||, <u, f>, <u, w> for a seeded Gaussian w and
+u at 4096 seeded positions (see ``u_probe``).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, "/root/reference/pkg/tests")
+sys.path.insert(0, REPO)
+
+import checkerhom as ch  # noqa: E402  (reference, read-only)
+from checkerhom.solver import make_preconditioner  # noqa: E402
+from checkerhom.spectral import regularized_inverse_diag  # noqa: E402
+
+from oracle import checkerhom_oracle as orc  # noqa: E402
+
+PROBE_SEED = 12345
+PROJ_SEED = 777
+N_PROBE = 4096
+
+
+def u_probe(u: np.ndarray, f: np.ndarray) -> dict:
+    N = u.size
+    idx = np.random.default_rng(PROBE_SEED).integers(0, N, size=N_PROBE)
+    w = np.random.default_rng(PROJ_SEED).standard_normal(N)
+    return {
+        "norm_u": float(np.linalg.norm(u)),
+        "u_dot_f": float(u @ f),
+        "u_dot_w": float(u @ w),
+        "probe_idx_seed": PROBE_SEED,
+        "proj_seed": PROJ_SEED,
+        "u_probe": [float(v) for v in u[idx]],
+        "sum_u": float(u.sum()),
+    }
+
+
+def ref_factors(n, d=3, eps=1e-8):
+    t = ch.dc_correction(ch.canonical_reciprocal(ch.fourier_eigenvalues(n), d, eps))
+    return np.stack(t.factors)
+
+
+def small():
+    out = {}
+    out["seeds_master0"] = np.array([ch.derive_seed(0, m) for m in range(256)], dtype=np.uint64)
+    out["seeds_master7"] = np.array([ch.derive_seed(7, m) for m in range(16)], dtype=np.uint64)
+    # LKR factors as produced by the reference setup (consumed as-is by the GPU path)
+    for n in (8, 16, 32, 64, 128, 256, 512):
+        fac = ref_factors(n)
+        if n <= 64:
+            out[f"factors_n{n}"] = fac
+        else:
+            # rows 0..R-1 are identical across the three modes; the last row is
+            # the dc fix (-origin at [0] on mode 0, 1 at [0] on modes 1, 2)
+            assert np.array_equal(fac[0, :-1], fac[1, :-1]) and np.array_equal(fac[0, :-1], fac[2, :-1])
+            assert np.count_nonzero(fac[1, -1]) == 1 and fac[1, -1, 0] == 1.0
+            out[f"factors_mode0_n{n}"] = fac[0]
+        out[f"eig_n{n}"] = ch.fourier_eigenvalues(n).values
+    out["factors2d_n8"] = np.stack(ch.dc_correction(
+        ch.canonical_reciprocal(ch.fourier_eigenvalues(8), 2, 1e-8)).factors)
+    q = ch.exp_sum_quadrature(1.0, 12.0, 1e-8)
+    out["quad_1_12_nodes"], out["quad_1_12_weights"] = q.nodes, q.weights
+
+    # realizations -> beta cell arrays
+    cases = []
+    cfgs = [
+        dict(d=3, L=2, n0=4, alpha="1/4", lam=0.4, seed=1),
+        dict(d=3, L=4, n0=4, alpha="1/4", lam=0.4, seed=2),
+        dict(d=3, L=4, n0=4, alpha="1/2", lam=0.1, seed=3),
+        dict(d=3, L=2, n0=8, alpha="1/4", lam=0.3, seed=4),
+        dict(d=3, L=4, n0=4, alpha="1/2", lam=0.2, seed=5,
+             contrast=ch.ContrastModel.two_value(0.3, 0.7)),
+        dict(d=3, L=4, n0=4, alpha="1/4", lam=0.2, seed=6,
+             contrast=ch.ContrastModel.layered([0.1, 0.5, 0.8]), subcell_offset=0),
+        dict(d=3, L=8, n0=4, alpha="1/2", lam=0.1, seed=int(out["seeds_master0"][0])),
+        dict(d=3, L=8, n0=4, alpha="1/2", lam=0.01, seed=int(out["seeds_master0"][1])),
+    ]
+    rng = np.random.default_rng(2024)
+    for ci, kw in enumerate(cfgs):
+        kw = dict(kw)
+        seed = kw.pop("seed")
+        cfg = ch.LatticeConfig(**kw)
+        r = ch.sample_realization(cfg, seed)
+        L, d = cfg.L, cfg.d
+        beta = np.zeros((L,) * d)
+        for c, b in r.cell_beta.items():
+            beta[c] = b
+        A = ch.assemble_stiffness(r)
+        n = cfg.n
+        x = np.random.default_rng(1000 + ci).standard_normal(n ** d)
+        y = A.matrix() @ x
+        pre = f"case{ci}_"
+        out[pre + "meta"] = np.array([d, L, cfg.n0, cfg.k, cfg.offset, seed % (2**62)], dtype=np.int64)
+        out[pre + "lam"] = np.array(cfg.lam)
+        out[pre + "beta"] = beta
+        out[pre + "Ax"] = y
+        for i in (1, 2, 3):
+            out[pre + f"rhs{i}"] = ch.corrector_rhs(r, i)
+        out[pre + "coef"] = ch.coefficient_grid(r).values
+        print("case", ci, cfg.n, r.num_covered, flush=True)
+
+    # preconditioner applies
+    for n in (8, 16, 32):
+        t = ch.dc_correction(ch.canonical_reciprocal(ch.fourier_eigenvalues(n), 3, 1e-8))
+        x = rng.standard_normal(n ** 3)
+        out[f"lkr_x_n{n}"] = x
+        out[f"lkr_y_n{n}"] = ch.apply_lkr_preconditioner(t, x)
+        gp = ch.pseudoinverse_diag(ch.eigensum_tensor(3, ch.fourier_eigenvalues(n)))
+        out[f"fourier_y_n{n}"] = ch.apply_fourier_preconditioner(gp, x)
+        rd = regularized_inverse_diag(ch.eigensum_tensor(3, ch.fourier_eigenvalues(n)), 1e-3)
+        out[f"reg_y_n{n}"] = ch.apply_fourier_preconditioner(rd, x)
+
+    # small PCG solves through the reference public API
+    pcg_cases = [
+        dict(L=2, n0=4, alpha="1/4", lam=0.4, seed=0, tol=1e-7, pre="lkr"),
+        dict(L=4, n0=4, alpha="1/4", lam=0.4, seed=1, tol=1e-7, pre="lkr"),
+        dict(L=4, n0=4, alpha="1/4", lam=0.4, seed=2, tol=1e-10, pre="fourier"),
+        dict(L=4, n0=4, alpha="1/2", lam=0.1, seed=3, tol=1e-9, pre="regularized"),
+        dict(L=4, n0=4, alpha="1/2", lam=0.1, seed=4, tol=1e-9, pre="lkr", prs=True),
+        dict(L=4, n0=4, alpha="1/4", lam=0.4, seed=5, tol=1e-30, pre="lkr", max_iter=3),
+    ]
+    for pi, kw in enumerate(pcg_cases):
+        cfg = ch.LatticeConfig(d=3, L=kw["L"], n0=kw["n0"], alpha=kw["alpha"], lam=kw["lam"])
+        r = ch.sample_realization(cfg, kw["seed"])
+        A = ch.assemble_stiffness(r)
+        h = 1.0 / cfg.n
+        f = (h ** (2 - 3)) * ch.corrector_rhs(r, 1)
+        opts = ch.SolveOptions(tol=kw["tol"], preconditioner=kw["pre"], eps_rank=1e-8,
+                               delta=1e-3 if kw["pre"] == "regularized" else 0.0,
+                               precond_residual_stopping=kw.get("prs", False),
+                               max_iter=kw.get("max_iter", 500))
+        u, rep = ch.pcg_solve(A, f, opts)
+        beta = np.zeros((cfg.L,) * 3)
+        for c, b in r.cell_beta.items():
+            beta[c] = b
+        pre = f"pcg{pi}_"
+        out[pre + "meta"] = np.array([cfg.L, cfg.n0, cfg.k, cfg.offset, rep.iterations,
+                                      int(rep.converged), int(kw.get("prs", False)),
+                                      kw.get("max_iter", 500)], dtype=np.int64)
+        out[pre + "lam_tol"] = np.array([cfg.lam, kw["tol"]])
+        out[pre + "kind"] = np.array(kw["pre"])
+        out[pre + "beta"] = beta
+        out[pre + "f"] = f
+        out[pre + "u"] = u
+        out[pre + "res"] = np.array(rep.residuals)
+        out[pre + "name"] = np.array(rep.preconditioner)
+        print("pcg", pi, rep.iterations, rep.converged, rep.preconditioner, flush=True)
+
+    # config 1 (n=32): full u for m = 0, 1
+    for m in (0, 1):
+        rec, u, f = config_run(1, m)
+        out[f"cfg1_m{m}_u"] = u
+        out[f"cfg1_m{m}_res"] = np.array(rec["residuals"])
+        out[f"cfg1_m{m}_its"] = np.array(rec["iterations"])
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **out)
+    print("wrote small.npz", os.path.getsize(os.path.join(HERE, "small.npz")))
+
+
+def config_run(cfg_id: int, m: int):
+    c = orc.CONFIGS[cfg_id]
+    seed = ch.derive_seed(0, m)
+    cfg = ch.LatticeConfig(d=3, L=c["L"], n0=c["n0"], alpha="1/2", lam=c["lam"])
+    r = ch.sample_realization(cfg, seed)
+    n = cfg.n
+    h = 1.0 / n
+    t0 = time.perf_counter()
+    if cfg_id == 5:
+        beta = np.zeros((cfg.L,) * 3)
+        for cc, b in r.cell_beta.items():
+            beta[cc] = b
+        k, off = cfg.k, cfg.offset
+        F = orc.cell_field(beta, cfg.n0, k, off)
+
+        class MF:
+            d = 3
+
+        A = MF()
+        A.n = n
+        sm = orc.StencilMatrix(F, cfg.lam)
+        A.matrix = lambda: sm
+        del F
+    else:
+        A = ch.assemble_stiffness(r)
+        A.matrix()
+    t_asm = time.perf_counter() - t0
+    if c["rhs"] == "corrector":
+        f = (h ** (2 - 3)) * ch.corrector_rhs(r, 1)
+    else:
+        f = np.random.default_rng(seed).standard_normal(n ** 3)
+        f -= f.mean()
+    opts = ch.SolveOptions(tol=c["tol"], preconditioner="lkr", eps_rank=1e-8)
+    P = make_preconditioner(3, n, opts)
+    t0 = time.perf_counter()
+    u, rep = ch.pcg_solve(A, f, opts, precond=P)
+    t_solve = time.perf_counter() - t0
+    rec = {"config": cfg_id, "m": m, "seed": str(seed), "n": n,
+           "iterations": rep.iterations, "converged": rep.converged,
+           "residuals": list(rep.residuals), "final_residual": rep.final_residual,
+           "preconditioner": rep.preconditioner, "rhs_projected": rep.rhs_projected,
+           "norm_f": float(np.linalg.norm(f)), "num_covered": r.num_covered,
+           "t_assembly_s": t_asm, "t_solve_s": t_solve}
+    rec.update(u_probe(u, f))
+    return rec, u, f
+
+
+def configs(cfg_id: int, start: int, count: int):
+    recs = []
+    path = os.path.join(HERE, f"config{cfg_id}_{start}_{count}.json")
+    for m in range(start, start + count):
+        rec, _, _ = config_run(cfg_id, m)
+        recs.append(rec)
+        print(cfg_id, m, rec["iterations"], rec["t_solve_s"], flush=True)
+        with open(path, "w") as fh:
+            json.dump({"generator": "tests/golden/make_golden.py (reference checkerhom)",
+                       "numpy": np.__version__, "records": recs}, fh, indent=1)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "small":
+        small()
+    else:
+        configs(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]))

@@ -1,0 +1,256 @@
+"""CUDA path vs the oracle and the reference's golden vectors (needs a B200).
+
+Every call goes through the C ABI (libchkpcg.so) via the package's ctypes
+binding.  Bars: integer results (iteration counts) exact; residual histories
+1e-8 relative; solutions 1e-9 relative L2 (north_star), operators 1e-13
+relative (fp64 roundoff of a different summation order).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import checkerhom_oracle as orc
+
+from conftest import golden_configs, golden_small
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2007_06524_b200 as chk  # noqa: E402
+from paper_2007_06524_b200 import _lib  # noqa: E402
+
+
+def _case_ids(prefix):
+    g = golden_small()
+    return sorted({k.split("_")[0] for k in g.files if k.startswith(prefix)})
+
+
+def _cfg_from_case(g, case):
+    d, L, n0, k, off, _ = (int(v) for v in g[case + "_meta"])
+    lam = float(g[case + "_lam"])
+    alpha = f"{k}/{2 * n0}"
+    cfg = chk.LatticeConfig(d=3, L=L, n0=n0, alpha=alpha, lam=lam, subcell_offset=off)
+    assert cfg.k == k and cfg.offset == off
+    return cfg
+
+
+def test_library_is_native():
+    lib = _lib.load()
+    assert lib.chk_abi_version() == 1
+
+
+@pytest.mark.parametrize("case", _case_ids("case"))
+def test_stencil_matches_reference_csr(case):
+    """chk_stencil_apply vs the reference CSR product (operators.py:122-131)."""
+    g = golden_small()
+    cfg = _cfg_from_case(g, case)
+    n = cfg.n
+    ci = int(case[4:])
+    x = np.random.default_rng(1000 + ci).standard_normal(n ** 3)
+    A = chk.StiffnessBatch(cfg, g[case + "_beta"].reshape(1, -1))
+    y, xy = A.matvec(torch.as_tensor(x).reshape(1, -1), with_dot=True)
+    y = y.cpu().numpy().ravel()
+    ref = g[case + "_Ax"]
+    assert np.linalg.norm(y - ref) <= 1e-14 * np.linalg.norm(ref)
+    assert abs(float(xy[0]) - x @ ref) <= 1e-12 * abs(x @ ref)
+
+
+@pytest.mark.parametrize("case", _case_ids("case"))
+def test_corrector_rhs_matches_reference(case):
+    g = golden_small()
+    cfg = _cfg_from_case(g, case)
+    A = chk.StiffnessBatch(cfg, g[case + "_beta"].reshape(1, -1))
+    for i in (1, 2, 3):
+        f = chk.corrector_rhs_batched(A, i, pcg_scaled=False).cpu().numpy().ravel()
+        assert np.allclose(f, g[case + f"_rhs{i}"], rtol=0, atol=1e-17)
+
+
+@pytest.mark.parametrize("n", [8, 16, 32])
+def test_preconditioner_apply_golden(n):
+    """chk_precond_apply vs reference apply_lkr / apply_fourier outputs."""
+    g = golden_small()
+    x = g[f"lkr_x_n{n}"]
+    t = chk.dc_correction(chk.canonical_reciprocal(chk.fourier_eigenvalues(n), 3, 1e-8))
+    y = chk.apply_lkr_preconditioner(t, x)
+    ref = g[f"lkr_y_n{n}"]
+    assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+    yf = chk.apply_fourier_preconditioner(n, x)
+    assert np.linalg.norm(yf - g[f"fourier_y_n{n}"]) <= 1e-13 * np.linalg.norm(yf)
+    yr = chk.apply_fourier_preconditioner(n, x, delta=1e-3)
+    assert np.linalg.norm(yr - g[f"reg_y_n{n}"]) <= 1e-13 * np.linalg.norm(yr)
+
+
+@pytest.mark.parametrize("n", [64, 128, 256])
+def test_preconditioner_apply_vs_oracle(n):
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((2, n ** 3))
+    fac = orc.lkr_factors(n)
+    t = chk.CanonicalTensor(3, n, fac)
+    y = chk.apply_lkr_preconditioner(t, torch.as_tensor(x).cuda()).cpu().numpy()
+    dg = orc.lkr_diagonal(fac)
+    for b in range(2):
+        ref = orc.apply_lkr(fac, x[b], dg)
+        # white-noise input: fp64 FFT roundoff (~1e-16 ||x||) is amplified by
+        # max D ~ n^2/(4 pi^2) relative to ||z||; both sides carry it
+        assert np.linalg.norm(y[b] - ref) <= 2e-12 * np.linalg.norm(ref)
+
+
+def test_preconditioner_properties_n512():
+    """n = 512: linearity, symmetry <Px, y> = <x, Py>, constants annihilated."""
+    n = 512
+    t = chk.dc_correction(chk.canonical_reciprocal(chk.fourier_eigenvalues(n), 3, 1e-8))
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(n ** 3, dtype=torch.float64, device="cuda", generator=gen)
+    y = torch.randn(n ** 3, dtype=torch.float64, device="cuda", generator=gen)
+    px = chk.apply_lkr_preconditioner(t, x)
+    py = chk.apply_lkr_preconditioner(t, y)
+    pxy = chk.apply_lkr_preconditioner(t, 1.7 * x + y)
+    assert torch.linalg.norm(pxy - (1.7 * px + py)) <= 1e-12 * torch.linalg.norm(pxy)
+    lhs, rhs = float(px @ y), float(x @ py)
+    assert abs(lhs - rhs) <= 1e-10 * float(torch.linalg.norm(x) * torch.linalg.norm(y))
+    one = torch.ones(n ** 3, dtype=torch.float64, device="cuda")
+    assert float(torch.linalg.norm(chk.apply_lkr_preconditioner(t, one))) <= 10 * 1e-8 * n ** 1.5
+    del x, y, px, py, pxy, one
+
+
+@pytest.mark.parametrize("pid", _case_ids("pcg"))
+def test_pcg_small_golden(pid):
+    """Reference pcg_solve outputs (incl. fourier / regularized / precond-residual
+    stopping / non-convergence) reproduced through the batched C ABI."""
+    g = golden_small()
+    L, n0, k, off, its, conv, prs, max_iter = (int(v) for v in g[pid + "_meta"])
+    lam, tol = (float(v) for v in g[pid + "_lam_tol"])
+    kind = str(g[pid + "_kind"])
+    cfg = chk.LatticeConfig(d=3, L=L, n0=n0, alpha=f"{k}/{2 * n0}", lam=lam, subcell_offset=off)
+    r = chk.realization_from_beta(cfg, g[pid + "_beta"])
+    A = chk.assemble_stiffness(r)
+    opts = chk.SolveOptions(tol=tol, preconditioner=kind, eps_rank=1e-8,
+                            delta=1e-3 if kind == "regularized" else 0.0,
+                            precond_residual_stopping=bool(prs), max_iter=max_iter)
+    u, rep = chk.pcg_solve(A, g[pid + "_f"], opts)
+    assert rep.iterations == its
+    assert rep.converged == bool(conv)
+    assert rep.preconditioner == str(g[pid + "_name"])
+    assert np.allclose(rep.residuals, g[pid + "_res"], rtol=1e-8, atol=0)
+    uref = g[pid + "_u"]
+    assert np.linalg.norm(u - uref) <= 1e-9 * np.linalg.norm(uref)
+
+
+@pytest.mark.parametrize("m", [0, 1])
+def test_config1_full_solution(m):
+    g = golden_small()
+    _, F, f = orc.config_problem(1, m)
+    cfg = chk.LatticeConfig(d=3, L=8, n0=4, alpha="1/2", lam=0.1)
+    r = chk.sample_realization(cfg, chk.derive_seed(0, m))
+    u, rep = chk.pcg_solve(chk.assemble_stiffness(r), f,
+                           chk.SolveOptions(tol=1e-8, preconditioner="lkr"))
+    assert rep.iterations == int(g[f"cfg1_m{m}_its"])
+    assert np.allclose(rep.residuals, g[f"cfg1_m{m}_res"], rtol=1e-8, atol=0)
+    uref = g[f"cfg1_m{m}_u"]
+    assert np.linalg.norm(u - uref) <= 1e-9 * np.linalg.norm(uref)
+
+
+def _probe_check(u, f, rec):
+    """Size-independent solution checks against the reference's u (golden probes)."""
+    N = u.size
+    norm_u = rec["norm_u"]
+    assert abs(np.linalg.norm(u) - norm_u) <= 1e-9 * norm_u
+    assert abs(u @ f - rec["u_dot_f"]) <= 1e-9 * norm_u * np.linalg.norm(f)
+    w = np.random.default_rng(rec["proj_seed"]).standard_normal(N)
+    assert abs(u @ w - rec["u_dot_w"]) <= 5e-9 * norm_u
+    idx = np.random.default_rng(rec["probe_idx_seed"]).integers(0, N, size=len(rec["u_probe"]))
+    probe = np.asarray(rec["u_probe"])
+    assert np.max(np.abs(u[idx] - probe)) <= 1e-9 * np.max(np.abs(probe)) * 10
+
+
+def _run_config(cfg_id, ms):
+    c = orc.CONFIGS[cfg_id]
+    cfg = chk.LatticeConfig(d=3, L=c["L"], n0=c["n0"], alpha="1/2", lam=c["lam"])
+    rs = [chk.sample_realization(cfg, chk.derive_seed(0, m)) for m in ms]
+    A = chk.StiffnessBatch(cfg, np.stack([r.beta_cells.ravel() for r in rs]))
+    if c["rhs"] == "corrector":
+        F = chk.corrector_rhs_batched(A, 1)
+    else:
+        F = torch.stack([torch.as_tensor(orc.gaussian_rhs(cfg.n, r.seed)) for r in rs]).cuda()
+    opts = chk.SolveOptions(tol=c["tol"], preconditioner="lkr", eps_rank=1e-8)
+    return F, chk.pcg_solve_batched(A, F, opts)
+
+
+@pytest.mark.parametrize("cfg_id,limit", [(2, 64), (3, 32), (4, 8), (5, 1)])
+def test_config_batched_vs_reference(cfg_id, limit):
+    """BASELINE configs through the realization batcher: the reference's
+    iteration counts exactly, residual histories, and the solution probes."""
+    recs = golden_configs(cfg_id)[:limit]
+    if not recs:
+        pytest.skip(f"config {cfg_id} golden not generated")
+    ms = [r["m"] for r in recs]
+    chunk = {2: 64, 3: 32, 4: 4, 5: 1}[cfg_id]
+    for s in range(0, len(ms), chunk):
+        sub = ms[s:s + chunk]
+        F, res = _run_config(cfg_id, sub)
+        for j, m in enumerate(sub):
+            rec = recs[s + j]
+            assert res.status[j] == 0
+            assert int(res.iterations[j]) == rec["iterations"], (m, res.iterations[j], rec["iterations"])
+            its = rec["iterations"]
+            assert np.allclose(res.history[j, :its], rec["residuals"], rtol=1e-7, atol=0)
+            u = res.u[j].cpu().numpy()
+            f = F[j].cpu().numpy()
+            _probe_check(u, f, rec)
+        del F, res
+        torch.cuda.empty_cache()
+
+
+def test_true_residual_and_mean_zero_n256():
+    """Full-size properties: ||f - A u|| / ||f|| tracks the recursive residual
+    (test_solver.py:99-103) and u is mean-zero."""
+    F, res = _run_config(4, [0])
+    c = orc.CONFIGS[4]
+    cfg = chk.LatticeConfig(d=3, L=c["L"], n0=c["n0"], alpha="1/2", lam=c["lam"])
+    r = chk.sample_realization(cfg, chk.derive_seed(0, 0))
+    A = chk.StiffnessBatch(cfg, r.beta_cells.reshape(1, -1))
+    Au = A.matvec(res.u)
+    rel = float(torch.linalg.norm(F - Au) / torch.linalg.norm(F))
+    assert rel <= 2.0 * float(res.final_residual[0]) + 1e-15
+    assert abs(float(res.u.mean())) <= 1e-12 * float(res.u.abs().max())
+
+
+def test_zero_rhs_and_mean_projection():
+    cfg = chk.LatticeConfig(d=3, L=4, n0=4, alpha="1/4", lam=0.4)
+    r = chk.sample_realization(cfg, 4)
+    A = chk.assemble_stiffness(r)
+    u, rep = chk.pcg_solve(A, np.zeros(cfg.n ** 3), chk.SolveOptions(preconditioner="lkr"))
+    assert rep.converged and rep.iterations == 0 and not u.any()
+    f = (1.0 / cfg.n) ** -1 * chk.corrector_rhs(r, 1)
+    with pytest.warns(UserWarning):
+        u1, rep1 = chk.pcg_solve(A, f + 1.0, chk.SolveOptions(tol=1e-8, preconditioner="lkr"))
+    assert rep1.rhs_projected
+    u2, _ = chk.pcg_solve(A, f, chk.SolveOptions(tol=1e-8, preconditioner="lkr"))
+    assert np.allclose(u1, u2, atol=1e-8)
+
+
+def test_nonconvergence_reported_and_breakdown_raised():
+    cfg = chk.LatticeConfig(d=3, L=4, n0=4, alpha="1/4", lam=0.4)
+    r = chk.sample_realization(cfg, 7)
+    A = chk.assemble_stiffness(r)
+    f = cfg.n * chk.corrector_rhs(r, 1)
+    _, rep = chk.pcg_solve(A, f, chk.SolveOptions(tol=1e-30, max_iter=2, preconditioner="lkr"))
+    assert not rep.converged and rep.iterations == 2 and rep.final_residual > 1e-30
+    # an indefinite operator (negative contrast) makes p'Ap <= 0: SolverBreakdown
+    bad = chk.realization_from_beta(cfg, -5.0 * np.ones((4, 4, 4)))
+    with pytest.raises(chk.SolverBreakdown):
+        chk.pcg_solve(chk.assemble_stiffness(bad), f, chk.SolveOptions(preconditioner="lkr"))
+
+
+def test_size_mismatch_raises_value_error():
+    t = chk.dc_correction(chk.canonical_reciprocal(chk.fourier_eigenvalues(8), 3, 1e-8))
+    with pytest.raises(ValueError):
+        chk.apply_lkr_preconditioner(t, np.ones(10))
+    cfg = chk.LatticeConfig(d=3, L=3, n0=4, lam=0.4)  # n = 12: not a power of two
+    with pytest.raises(ValueError):
+        chk.pcg_solve(chk.assemble_stiffness(chk.sample_realization(cfg, 1)), np.ones(12 ** 3))

@@ -1,0 +1,115 @@
+"""Host-side logic and the C ABI surface (no GPU needed)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import REPO, golden_small
+
+import paper_2007_06524_b200 as chk
+from paper_2007_06524_b200 import _lib
+
+
+def _header_symbols():
+    text = open(os.path.join(REPO, "include", "chk_pcg.h")).read()
+    return sorted(set(re.findall(r"\b(chk_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    lib = _lib.load()
+    declared = _header_symbols()
+    assert len(declared) >= 10
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(_lib.SIGNATURES), "ctypes binding out of sync with chk_pcg.h"
+    assert lib.chk_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_abi_rejects_bad_arguments_without_gpu():
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    assert lib.chk_precond_plan_create(1, 12, 5, None, None, 0.0, ctypes.byref(h)) == _lib.CHK_EUNSUPPORTED
+    assert lib.chk_precond_plan_create(7, 16, 5, None, None, 0.0, ctypes.byref(h)) == _lib.CHK_EINVAL
+    g = _lib.ChkGrid(2, 16, 4, 4, 2, 1, 0.4)
+    assert lib.chk_stencil_apply(ctypes.byref(g), None, None, None, None, 1, None) == _lib.CHK_EUNSUPPORTED
+    with pytest.raises(ValueError):
+        _lib.check(_lib.CHK_EINVAL)
+    assert lib.chk_pcg_workspace_bytes(ctypes.byref(g), None, 1, 10) == 0
+
+
+def test_sampling_bit_identical_to_reference():
+    g = golden_small()
+    for m in range(256):
+        assert chk.derive_seed(0, m) == int(g["seeds_master0"][m])
+    cfg = chk.LatticeConfig(d=3, L=8, n0=4, alpha="1/2", lam=0.1)
+    r = chk.sample_realization(cfg, chk.derive_seed(0, 0))
+    assert np.array_equal(r.beta_cells, g["case6_beta"])
+    cfg2 = chk.LatticeConfig(d=3, L=4, n0=4, alpha="1/2", lam=0.2,
+                             contrast=chk.ContrastModel.two_value(0.3, 0.7))
+    assert np.array_equal(chk.sample_realization(cfg2, 5).beta_cells, g["case4_beta"])
+    cfg3 = chk.LatticeConfig(d=3, L=4, n0=4, alpha="1/4", lam=0.2,
+                             contrast=chk.ContrastModel.layered([0.1, 0.5, 0.8]), subcell_offset=0)
+    assert np.array_equal(chk.sample_realization(cfg3, 6).beta_cells, g["case5_beta"])
+
+
+def test_coefficient_grid_matches_reference():
+    g = golden_small()
+    cfg = chk.LatticeConfig(d=3, L=4, n0=4, alpha="1/4", lam=0.4)
+    r = chk.sample_realization(cfg, 2)
+    assert np.allclose(chk.coefficient_grid(r), g["case1_coef"], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("n", [8, 16, 32, 64, 128, 256, 512])
+def test_device_plan_factors_bit_identical(n):
+    """The factors the GPU plan consumes equal the reference setup's."""
+    g = golden_small()
+    t = chk.dc_correction(chk.canonical_reciprocal(chk.fourier_eigenvalues(n), 3, 1e-8))
+    fac = np.stack(t.factors)
+    if n <= 64:
+        assert np.array_equal(fac, g[f"factors_n{n}"])
+    else:
+        assert np.array_equal(fac[0], g[f"factors_mode0_n{n}"])
+        assert np.array_equal(fac[2, :-1], g[f"factors_mode0_n{n}"][:-1])
+
+
+def test_solve_options_validation():
+    with pytest.raises(chk.ConfigurationError):
+        chk.SolveOptions(tol=0.0)
+    with pytest.raises(chk.ConfigurationError):
+        chk.SolveOptions(max_iter=0)
+    with pytest.raises(chk.ConfigurationError):
+        chk.SolveOptions(preconditioner="amg")
+    with pytest.raises(chk.ConfigurationError):
+        chk.SolveOptions(delta=-1.0)
+    assert issubclass(chk.ConfigurationError, ValueError)
+
+
+def test_lattice_validation():
+    with pytest.raises(chk.ConfigurationError):
+        chk.LatticeConfig(d=3, L=4, n0=6)
+    with pytest.raises(chk.ConfigurationError):
+        chk.LatticeConfig(d=3, L=4, n0=4, alpha="3/4")
+    with pytest.raises(chk.ConfigurationError):
+        chk.LatticeConfig(d=3, L=4, n0=4, lam=0.0)
+
+
+def test_no_oracle_import_in_product():
+    pkg = os.path.join(REPO, "paper_2007_06524_b200")
+    for root, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith(".py"):
+                text = open(os.path.join(root, fn)).read()
+                assert "oracle" not in re.sub(r"#.*", "", text).split("\"\"\"")[-1] or "import oracle" not in text
+                assert "from oracle" not in text and "import oracle" not in text
