@@ -97,22 +97,23 @@ int fail(int code, const std::string& msg) {
 // spectral columns per middle-pass tile.
 template <int N>
 struct Cfg;
-template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8;  };
-template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16; };
-template <> struct Cfg<32>  { static constexpr int G = 1,  W = 32; };
-template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16; };
-template <> struct Cfg<128> { static constexpr int G = 2,  W = 16; };
-template <> struct Cfg<256> { static constexpr int G = 8,  W = 2;  };
-template <> struct Cfg<512> { static constexpr int G = 16, W = 1;  };
+// NB realizations share one evaluation of the diagonal tile in the middle pass.
+template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8,  NB = 4; };
+template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16, NB = 4; };
+template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4; };
+template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 8; };
+template <> struct Cfg<128> { static constexpr int G = 2,  W = 8,  NB = 8; };
+template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 4; };
+template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2; };
 
 template <int N>
 struct Ops {
-  static constexpr int G = Cfg<N>::G, W = Cfg<N>::W, NR = N / G, H = N / 2 + 1;
+  static constexpr int G = Cfg<N>::G, W = Cfg<N>::W, NB = Cfg<N>::NB, NR = N / G, H = N / 2 + 1;
   static constexpr int TILES = NR * H / W;
   static constexpr int PLANE_BLOCKS = N * G;  // per realization
   static constexpr size_t plane_smem() { return (size_t)NR * H * sizeof(double2); }
   static size_t mid_smem(int r1) {
-    return (size_t)N * (G * W + 1) * sizeof(double2) + (size_t)r1 * G * W * sizeof(double);
+    return (size_t)mid_dsm_offset(N * (G * W + 1), G * W, r1) + (size_t)N * G * W * sizeof(double);
   }
   static int maxblk() { return PLANE_BLOCKS > TILES ? PLANE_BLOCKS : TILES; }
 
@@ -141,17 +142,24 @@ struct Ops {
     CHK_LAUNCHED();
     return CHK_OK;
   }
-  static int mid(int mode, cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it) {
+  template <int NBX, int MODE>
+  static int mid_launch(cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it) {
     const size_t sm = mid_smem(pl.kind == KIND_LKR ? pl.r1 : 0);
-    dim3 grid(B * TILES), block(256);
+    dim3 grid(((B + NBX - 1) / NBX) * TILES), block(256);
+    CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, NBX, MODE>, sm));
+    mid_column_kernel<N, G, W, NBX, MODE><<<grid, block, sm, s>>>(S, pl, ctl, it, B);
+    return CHK_OK;
+  }
+  static int mid(int mode, cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it) {
     ProfScope ps(2, s);
-    if (mode == MID_APPLY) {
-      CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, MID_APPLY>, sm));
-      mid_column_kernel<N, G, W, MID_APPLY><<<grid, block, sm, s>>>(S, pl, ctl, it);
-    } else {
-      CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, MID_PCG>, sm));
-      mid_column_kernel<N, G, W, MID_PCG><<<grid, block, sm, s>>>(S, pl, ctl, it);
-    }
+    // amortise the diagonal over NB realizations when that still fills the GPU
+    const bool wide = ((B + NB - 1) / NB) * TILES >= 2 * 148;
+    int rc;
+    if (mode == MID_APPLY)
+      rc = wide ? mid_launch<NB, MID_APPLY>(s, B, S, pl, ctl, it) : mid_launch<1, MID_APPLY>(s, B, S, pl, ctl, it);
+    else
+      rc = wide ? mid_launch<NB, MID_PCG>(s, B, S, pl, ctl, it) : mid_launch<1, MID_PCG>(s, B, S, pl, ctl, it);
+    if (rc) return rc;
     CHK_LAUNCHED();
     return CHK_OK;
   }
@@ -303,11 +311,27 @@ struct chk_precond_plan {
   double delta;
   double2* d_tw;
   double* d_U;
+  double* d_Up;
   double* d_lam;
 };
 
 static PlanDev plan_dev(const chk_precond_plan* p) {
-  return PlanDev{p->d_tw, p->d_U, p->d_lam, p->r1, p->kind, p->delta};
+  return PlanDev{p->d_tw, p->d_U, p->d_Up, p->d_lam, p->r1, p->kind, p->delta};
+}
+
+// host copy of dig_freq (chk_kernels.cuh): frequency stored at digit-reversed position p
+static int host_dig_freq(int N, int p) {
+  int k = 0, mul = 1, M = N;
+  while (M > 1) {
+    const int R = (M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2);
+    const int Mn = M / R;
+    const int m = p / Mn;
+    p -= m * Mn;
+    k += m * mul;
+    mul *= R;
+    M = Mn;
+  }
+  return k;
 }
 
 extern "C" {
@@ -347,7 +371,7 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
   if (kind != CHK_PRECOND_LKR && eigenvalues == nullptr)
     return fail(CHK_EINVAL, "Fourier plans need the eigenvalues");
   if (kind == CHK_PRECOND_REGULARIZED && delta < 0.0) return fail(CHK_EINVAL, "delta must be >= 0");
-  auto* p = new chk_precond_plan{kind, n, kind == CHK_PRECOND_LKR ? r1 : 0, delta, nullptr, nullptr, nullptr};
+  auto* p = new chk_precond_plan{kind, n, kind == CHK_PRECOND_LKR ? r1 : 0, delta, nullptr, nullptr, nullptr, nullptr};
   // twiddles w[k] = exp(-2 pi i k / n), octant-reduced for symmetric accuracy
   std::vector<double2> tw(n);
   for (int k = 0; k < n; ++k) {
@@ -368,6 +392,13 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
   if (kind == CHK_PRECOND_LKR) {
     if ((e = cudaMalloc(&p->d_U, sizeof(double) * 3 * (size_t)r1 * n)) != cudaSuccess) goto cuda_fail;
     if ((e = cudaMemcpy(p->d_U, factors, sizeof(double) * 3 * (size_t)r1 * n, cudaMemcpyHostToDevice)) != cudaSuccess) goto cuda_fail;
+    {
+      std::vector<double> up((size_t)r1 * n);
+      for (int r = 0; r < r1; ++r)
+        for (int q = 0; q < n; ++q) up[(size_t)r * n + q] = factors[(size_t)r * n + host_dig_freq(n, q)];
+      if ((e = cudaMalloc(&p->d_Up, sizeof(double) * up.size())) != cudaSuccess) goto cuda_fail;
+      if ((e = cudaMemcpy(p->d_Up, up.data(), sizeof(double) * up.size(), cudaMemcpyHostToDevice)) != cudaSuccess) goto cuda_fail;
+    }
   } else {
     if ((e = cudaMalloc(&p->d_lam, sizeof(double) * n)) != cudaSuccess) goto cuda_fail;
     if ((e = cudaMemcpy(p->d_lam, eigenvalues, sizeof(double) * n, cudaMemcpyHostToDevice)) != cudaSuccess) goto cuda_fail;
@@ -383,6 +414,7 @@ int32_t chk_precond_plan_destroy(chk_precond_plan* p) {
   if (!p) return CHK_OK;
   if (p->d_tw) cudaFree(p->d_tw);
   if (p->d_U) cudaFree(p->d_U);
+  if (p->d_Up) cudaFree(p->d_Up);
   if (p->d_lam) cudaFree(p->d_lam);
   delete p;
   return CHK_OK;
@@ -493,7 +525,6 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
       if ((rc2 = O::inv(INV_PCG, s, B, w.S, w.p, pl, ctl, 0))) return rc2;
       // iterations, polled every `chunk` with one chunk of look-ahead
       const int chunk = (n >= 128) ? 2 : 8;
-      int polled_upto = 0;
       bool pending = false;
       int ev_i = 0;
       for (int it = 1; it <= opts->max_iter; ++it) {
@@ -514,10 +545,8 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
           CHK_CUDA(cudaEventRecord(ev[ev_i], s));
           ev_i ^= 1;
           pending = true;
-          polled_upto = it;
         }
       }
-      (void)polled_upto;
       if ((rc2 = O::mean_u(s, B, u, ctl))) return rc2;
     });
     {

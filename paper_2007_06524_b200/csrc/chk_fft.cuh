@@ -89,16 +89,16 @@ struct Radix {
 // One in-place stage at sub-length M of a length-N transform over `npencil`
 // pencils; element e of pencil p is at buf[addr(p, e)].  Consecutive threads
 // take consecutive pencils (callers lay pencils out bank-conflict free).
-template <int N, int M, bool INV, class Addr>
-__device__ __forceinline__ void fft_stage(double2* buf, int npencil, const Addr& addr,
+template <int N, int M, bool INV, int NP, class Addr>
+__device__ __forceinline__ void fft_stage(double2* buf, const Addr& addr,
                                           const double2* __restrict__ tw, int twstride) {
   constexpr int R = Radix<M>::value;
   constexpr int S = M / R;
   constexpr int NBF = N / R;
-  const int total = npencil * NBF;
+  constexpr int total = NP * NBF;
   for (int w = threadIdx.x; w < total; w += blockDim.x) {
-    const int p = w % npencil;
-    const int bf = w / npencil;
+    const int p = w % NP;
+    const int bf = w / NP;
     const int blk = bf / S, j = bf - (bf / S) * S;
     const int base = blk * M + j;
     double2 v[R];
@@ -122,19 +122,19 @@ __device__ __forceinline__ void fft_stage(double2* buf, int npencil, const Addr&
   }
 }
 
-template <int N, int M, bool INV>
+template <int N, int M, bool INV, int NP>
 struct FftRec {
   template <class Addr>
-  __device__ __forceinline__ static void run(double2* buf, int npencil, const Addr& addr,
+  __device__ __forceinline__ static void run(double2* buf, const Addr& addr,
                                              const double2* __restrict__ tw, int twstride) {
     constexpr int R = Radix<M>::value;
     if constexpr (!INV) {
-      fft_stage<N, M, false>(buf, npencil, addr, tw, twstride);
+      fft_stage<N, M, false, NP>(buf, addr, tw, twstride);
       __syncthreads();
-      if constexpr (M / R > 1) FftRec<N, M / R, false>::run(buf, npencil, addr, tw, twstride);
+      if constexpr (M / R > 1) FftRec<N, M / R, false, NP>::run(buf, addr, tw, twstride);
     } else {
-      if constexpr (M / R > 1) FftRec<N, M / R, true>::run(buf, npencil, addr, tw, twstride);
-      fft_stage<N, M, true>(buf, npencil, addr, tw, twstride);
+      if constexpr (M / R > 1) FftRec<N, M / R, true, NP>::run(buf, addr, tw, twstride);
+      fft_stage<N, M, true, NP>(buf, addr, tw, twstride);
       __syncthreads();
     }
   }
@@ -143,10 +143,10 @@ struct FftRec {
 // Full length-N transform; the caller must __syncthreads() before (data in
 // smem); returns after a __syncthreads().  Forward: natural -> digit-reversed.
 // Inverse (unnormalised): digit-reversed -> natural, result scaled by N.
-template <int N, bool INV, class Addr>
-__device__ __forceinline__ void fft_smem(double2* buf, int npencil, const Addr& addr,
+template <int N, bool INV, int NP, class Addr>
+__device__ __forceinline__ void fft_smem(double2* buf, const Addr& addr,
                                          const double2* __restrict__ tw, int ntab) {
-  if constexpr (N > 1) FftRec<N, N, INV>::run(buf, npencil, addr, tw, ntab / N);
+  if constexpr (N > 1) FftRec<N, N, INV, NP>::run(buf, addr, tw, ntab / N);
 }
 
 // ----------------------------------------------------------------------------

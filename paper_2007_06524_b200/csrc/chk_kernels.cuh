@@ -67,6 +67,7 @@ struct SolveCtl {
 struct PlanDev {
   const double2* tw;  // [n] exp(-2 pi i k / n)
   const double* U;    // [3][r1][n] (LKR)
+  const double* Up;   // [r1][n] U0 with columns in digit-reversed order (LKR)
   const double* lam;  // [n] eigenvalues (FOURIER / REGULARIZED)
   int r1;
   int kind;
@@ -152,40 +153,98 @@ __device__ __forceinline__ double fcell(const double* __restrict__ beta, const G
   return in ? __ldg(beta + ((j0 >> g.sh) * g.L + (j1 >> g.sh)) * g.L + (j2 >> g.sh)) : 0.0;
 }
 
-// (A p)_x for node x of one realization (p, beta already offset).
+// Per-row context of the stencil for row (x0, x1) of one realization.
+struct RowCtx {
+  const double* pc;      // p(x0,   x1,   :)
+  const double* pxm;     // p(x0-1, x1,   :)
+  const double* pxp;     // p(x0+1, x1,   :)
+  const double* pym;     // p(x0,   x1-1, :)
+  const double* pyp;     // p(x0,   x1+1, :)
+  const double* bab[4];  // beta row of cells (c(j0), c(j1), :) for (j0, j1) in
+                         // {(x0-1,x1-1), (x0-1,x1), (x0,x1-1), (x0,x1)}; null = outside sub-cell
+};
+
+__device__ __forceinline__ RowCtx make_row(const double* __restrict__ p, const double* __restrict__ beta,
+                                           const Geo& g, int x0, int x1) {
+  const int n = g.n, nm = n - 1;
+  const size_t nn = (size_t)n * n;
+  const int a0 = (x0 - 1) & nm, p0 = (x0 + 1) & nm, a1 = (x1 - 1) & nm, p1 = (x1 + 1) & nm;
+  RowCtx rc;
+  rc.pc = p + (size_t)x0 * nn + (size_t)x1 * n;
+  rc.pxm = p + (size_t)a0 * nn + (size_t)x1 * n;
+  rc.pxp = p + (size_t)p0 * nn + (size_t)x1 * n;
+  rc.pym = p + (size_t)x0 * nn + (size_t)a1 * n;
+  rc.pyp = p + (size_t)x0 * nn + (size_t)p1 * n;
+  const int j0[2] = {a0, x0}, j1[2] = {a1, x1};
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const bool in = ((unsigned)((j0[a] & g.mask) - g.off) < (unsigned)g.k) &&
+                      ((unsigned)((j1[b] & g.mask) - g.off) < (unsigned)g.k);
+      rc.bab[a * 2 + b] = in ? beta + ((size_t)(j0[a] >> g.sh) * g.L + (j1[b] >> g.sh)) * g.L : nullptr;
+    }
+  return rc;
+}
+
+__device__ __forceinline__ void ld4(const double* __restrict__ p, double (&v)[4]) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
+// (A p)_x for the 4 nodes x2 = x2s .. x2s+3 (x2s % 4 == 0) of one row:
 //   g_a(x) = lam + 1/4 sum_{delta} F[h-cell x_a, transverse x_b - delta_b]
 //   (A p)_x = sum_a g_a(x)(p_x - p_{x+e_a}) + g_a(x-e_a)(p_x - p_{x-e_a})
 // (tests/oracles.py:52-75; transverse delta order of the reference loop).
-__device__ __forceinline__ double stencil_node(const double* __restrict__ p,
-                                               const double* __restrict__ beta, const Geo& g,
-                                               int x0, int x1, int x2, double& pc) {
-  const int n = g.n, nm = n - 1;
-  const int a0 = (x0 - 1) & nm, a1 = (x1 - 1) & nm, a2 = (x2 - 1) & nm;
-  const int p0 = (x0 + 1) & nm, p1 = (x1 + 1) & nm, p2 = (x2 + 1) & nm;
-  // F[a][b][c], a: {x0-1, x0}, b: {x1-1, x1}, c: {x2-1, x2}
-  const double f000 = fcell(beta, g, a0, a1, a2), f001 = fcell(beta, g, a0, a1, x2);
-  const double f010 = fcell(beta, g, a0, x1, a2), f011 = fcell(beta, g, a0, x1, x2);
-  const double f100 = fcell(beta, g, x0, a1, a2), f101 = fcell(beta, g, x0, a1, x2);
-  const double f110 = fcell(beta, g, x0, x1, a2), f111 = fcell(beta, g, x0, x1, x2);
+// n0 >= 4 and x2s % 4 == 0 put x2s..x2s+3 in one cell, so each of the four
+// (j0, j1) cell rows needs two beta loads for the five h-cells x2s-1..x2s+3.
+__device__ __forceinline__ void stencil4(const Geo& g, const RowCtx& rc, int x2s, double (&pc)[4],
+                                         double (&q)[4]) {
+  const int nm = g.n - 1;
+  double xm[4], xp[4], ym[4], yp[4];
+  ld4(rc.pc + x2s, pc);
+  ld4(rc.pxm + x2s, xm);
+  ld4(rc.pxp + x2s, xp);
+  ld4(rc.pym + x2s, ym);
+  ld4(rc.pyp + x2s, yp);
+  const double pl = __ldg(rc.pc + ((x2s - 1) & nm));
+  const double pr = __ldg(rc.pc + ((x2s + 4) & nm));
+  const int jm = (x2s - 1) & nm;
+  const bool inm = (unsigned)((jm & g.mask) - g.off) < (unsigned)g.k;
+  bool in[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) in[i] = (unsigned)(((x2s + i) & g.mask) - g.off) < (unsigned)g.k;
+  double f[4][5];
+#pragma unroll
+  for (int ab = 0; ab < 4; ++ab) {
+    const double* br = rc.bab[ab];
+    const double bm = (br && inm) ? __ldg(br + (jm >> g.sh)) : 0.0;
+    const double b0 = br ? __ldg(br + (x2s >> g.sh)) : 0.0;
+    f[ab][0] = bm;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[ab][i + 1] = in[i] ? b0 : 0.0;
+  }
   const double lam = g.lam;
-  // axis 0 edge x->x+e0: h-cell j0 = x0, delta over (x1, x2)
-  const double g0p = lam + (((f111 + f110) + f101) + f100) * 0.25;
-  const double g0m = lam + (((f011 + f010) + f001) + f000) * 0.25;
-  // axis 1 edge: j1 = x1, delta over (x0, x2)
-  const double g1p = lam + (((f111 + f110) + f011) + f010) * 0.25;
-  const double g1m = lam + (((f101 + f100) + f001) + f000) * 0.25;
-  // axis 2 edge: j2 = x2, delta over (x0, x1)
-  const double g2p = lam + (((f111 + f101) + f011) + f001) * 0.25;
-  const double g2m = lam + (((f110 + f100) + f010) + f000) * 0.25;
-  const size_t nn = (size_t)n * n;
-  const size_t row = (size_t)x0 * nn + (size_t)x1 * n;
-  pc = __ldg(p + row + x2);
-  const double q0 = g0p * (pc - __ldg(p + (size_t)p0 * nn + (size_t)x1 * n + x2)) +
-                    g0m * (pc - __ldg(p + (size_t)a0 * nn + (size_t)x1 * n + x2));
-  const double q1 = g1p * (pc - __ldg(p + (size_t)x0 * nn + (size_t)p1 * n + x2)) +
-                    g1m * (pc - __ldg(p + (size_t)x0 * nn + (size_t)a1 * n + x2));
-  const double q2 = g2p * (pc - __ldg(p + row + p2)) + g2m * (pc - __ldg(p + row + a2));
-  return (q0 + q1) + q2;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    // F_{abc}: a in {x0-1, x0}, b in {x1-1, x1}, c in {x2-1, x2}
+    const double f000 = f[0][i], f001 = f[0][i + 1], f010 = f[1][i], f011 = f[1][i + 1];
+    const double f100 = f[2][i], f101 = f[2][i + 1], f110 = f[3][i], f111 = f[3][i + 1];
+    const double g0p = lam + (((f111 + f110) + f101) + f100) * 0.25;
+    const double g0m = lam + (((f011 + f010) + f001) + f000) * 0.25;
+    const double g1p = lam + (((f111 + f110) + f011) + f010) * 0.25;
+    const double g1m = lam + (((f101 + f100) + f001) + f000) * 0.25;
+    const double g2p = lam + (((f111 + f101) + f011) + f001) * 0.25;
+    const double g2m = lam + (((f110 + f100) + f010) + f000) * 0.25;
+    const double c = pc[i];
+    const double left = (i == 0) ? pl : pc[i - 1];
+    const double right = (i == 3) ? pr : pc[i + 1];
+    const double q0 = g0p * (c - xp[i]) + g0m * (c - xm[i]);
+    const double q1 = g1p * (c - yp[i]) + g1m * (c - ym[i]);
+    const double q2 = g2p * (c - right) + g2m * (c - left);
+    q[i] = (q0 + q1) + q2;
+  }
 }
 
 // Standalone matvec y = A x (+ optional <x, y>), CTA per (realization, x0, group).
@@ -203,13 +262,17 @@ __global__ void __launch_bounds__(256) stencil_apply_kernel(Geo g, const double*
   const double* xb = x + b * nb;
   const double* bb = beta + (size_t)b * g.L * g.L * g.L;
   double acc = 0.0;
-  for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
-    const int t = i / N, x2 = i - (i / N) * N;
+  constexpr int Q4 = N / 4;
+  for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
+    const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
     const int x1 = gg + G * t;
-    double pc;
-    const double q = stencil_node(xb, bb, g, x0, x1, x2, pc);
-    y[b * nb + ((size_t)x0 * N + x1) * N + x2] = q;
-    acc += pc * q;
+    const RowCtx rc = make_row(xb, bb, g, x0, x1);
+    double pc[4], q[4];
+    stencil4(g, rc, x2, pc, q);
+    double2* yo = reinterpret_cast<double2*>(y + b * nb + ((size_t)x0 * N + x1) * N + x2);
+    yo[0] = make_double2(q[0], q[1]);
+    yo[1] = make_double2(q[2], q[3]);
+    acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
   }
   if (xy != nullptr) {
     double t0, t1;
@@ -350,11 +413,13 @@ __global__ void __launch_bounds__(256) stencil_dot_kernel(Geo g, const double* _
   const double* pb = p + b * nb;
   const double* bb = beta + (size_t)b * g.L * g.L * g.L;
   double acc = 0.0;
-  for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
-    const int t = i / N, x2 = i - (i / N) * N;
-    double pc;
-    const double q = stencil_node(pb, bb, g, x0, gg + G * t, x2, pc);
-    acc += pc * q;
+  constexpr int Q4 = N / 4;
+  for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
+    const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
+    const RowCtx rc = make_row(pb, bb, g, x0, gg + G * t);
+    double pc[4], q[4];
+    stencil4(g, rc, x2, pc, q);
+    acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
   }
   double t0, t1;
   if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G, scratch,
@@ -430,17 +495,27 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
     const double* pb = src + b * nb;
     const double* bb = beta + (size_t)b * g.L * g.L * g.L;
     double acc = 0.0;
-    for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
-      const int t = i / N, x2 = i - (i / N) * N;
+    constexpr int Q4 = N / 4;
+    for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
+      const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
       const int x1 = gg + G * t;
       const size_t idx = b * nb + ((size_t)x0 * N + x1) * N + x2;
-      double pc;
-      const double q = stencil_node(pb, bb, g, x0, x1, x2, pc);
-      u[idx] = u[idx] + alpha * pc;           // solver.py:167
-      const double rv = r[idx] - alpha * q;   // solver.py:168
-      r[idx] = rv;
-      sm[t * 2 * HP + x2] = rv;
-      acc += rv * rv;
+      const RowCtx rc = make_row(pb, bb, g, x0, x1);
+      double pc[4], q[4];
+      stencil4(g, rc, x2, pc, q);
+      double2* u2 = reinterpret_cast<double2*>(u + idx);
+      double2* r2 = reinterpret_cast<double2*>(r + idx);
+      double2 ua = u2[0], ub = u2[1], ra = r2[0], rb = r2[1];
+      ua.x += alpha * pc[0]; ua.y += alpha * pc[1];   // solver.py:167
+      ub.x += alpha * pc[2]; ub.y += alpha * pc[3];
+      ra.x -= alpha * q[0]; ra.y -= alpha * q[1];     // solver.py:168
+      rb.x -= alpha * q[2]; rb.y -= alpha * q[3];
+      u2[0] = ua; u2[1] = ub;
+      r2[0] = ra; r2[1] = rb;
+      double2* s2 = reinterpret_cast<double2*>(sm + t * 2 * HP + x2);
+      s2[0] = ra;
+      s2[1] = rb;
+      acc += ((ra.x * ra.x + ra.y * ra.y) + rb.x * rb.x) + rb.y * rb.y;
     }
     double t0, t1;
     if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G,
@@ -467,11 +542,11 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
   }
   __syncthreads();
   // R2C along x2: rows of N reals viewed as N/2 complex (z_m = x_2m + i x_2m+1)
-  fft_smem<N2, false>(buf, NR, RowAddr{HP}, pl.tw, N);
+  fft_smem<N2, false, NR>(buf, RowAddr{HP}, pl.tw, N);
   r2c_post<N>(buf, NR, HP, pl.tw);
   __syncthreads();
   // C2C along the x1 group (length NR)
-  fft_smem<NR, false>(buf, H, ColAddr{HP}, pl.tw, N);
+  fft_smem<NR, false, H>(buf, ColAddr{HP}, pl.tw, N);
   double2* dst = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
   for (int i = threadIdx.x; i < NR * H; i += blockDim.x) dst[i] = buf[i];
 }
@@ -481,26 +556,47 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
 // ----------------------------------------------------------------------------
 enum : int { MID_APPLY = 0, MID_PCG = 1 };
 
-template <int N, int G, int W, int MODE>
+__host__ __device__ __forceinline__ int mid_dsm_offset(int tile_elems, int gw, int r1) {
+  const int a = tile_elems * 16, c = r1 * gw * 8;
+  return ((a > c ? a : c) + 15) & ~15;
+}
+
+// A CTA owns W consecutive spectral columns c' of every (x0, group) slab and
+// NB realizations.  The diagonal tile D[pos0][slot] (N x G*W) is evaluated once
+// per CTA -- LKR: D = U0p^T C with C[r][slot] = U1[r][k1] U2[r][k2] (a rank-r1
+// contraction; U0p = U0 with columns in digit-reversed x0 order, so a thread's
+// 4 consecutive pos0 are contiguous) -- and reused for the NB realizations.
+template <int N, int G, int W, int NB, int MODE>
 __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S, PlanDev pl,
-                                                         SolveCtl ctl, int it) {
+                                                         SolveCtl ctl, int it, int B) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
   constexpr int TILES = NR * H / W;
   constexpr int GW = G * W;
   constexpr int RS = GW + 1;
-  extern __shared__ double2 buf[];
+  extern __shared__ double2 buf[];  // [N][RS] data tile (aliased by the [r1][GW] coefficients)
+  const int doff = mid_dsm_offset(N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
+  double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
   __shared__ double scratch[32];
   __shared__ int s_k1[GW], s_k2[GW];
-  const int b = blockIdx.x / TILES;
-  const int tile = blockIdx.x - b * TILES;
+  __shared__ double2 s_tw[GW];
+  __shared__ int s_any;
+  const int bg = blockIdx.x / TILES;
+  const int tile = blockIdx.x - bg * TILES;
   const int c0 = tile * W;
-  RState* st = (MODE == MID_PCG) ? ctl.st + b : nullptr;
-  if (MODE == MID_PCG && st->status != ST_ACTIVE) return;
-  double* coef = reinterpret_cast<double*>(buf + N * RS);  // [r1][GW] (LKR)
+  const int b0 = bg * NB;
 
-  // column bookkeeping: slot s = m*W + w  <->  (k1, k2)
+  if (MODE == MID_PCG) {
+    if (threadIdx.x == 0) {
+      int any = 0;
+      for (int j = 0; j < NB && b0 + j < B; ++j) any |= (ctl.st[b0 + j].status == ST_ACTIVE);
+      s_any = any;
+    }
+    __syncthreads();
+    if (!s_any) return;
+  }
+  // slot s = m*W + w  <->  (k1, k2); group-combine twiddle w_n^(g k') per (g, w)
   for (int s = threadIdx.x; s < GW; s += blockDim.x) {
     const int m = dig_freq<G>(s / W), w = s % W;
     const int c = c0 + w;
@@ -508,97 +604,124 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
     const int kp = dig_freq<NR>(q1);
     s_k1[s] = kp + m * NR;
     s_k2[s] = (q2 == N2) ? N2 : dig_freq<N2>(q2);
-  }
-  // load the tile; apply the group-combine twiddle w_n^(g k') on the fly
-  const double2* src = S + (size_t)b * N * G * (NR * H);
-  for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
-    const int w = i % W, gq = (i / W) % G, x0 = i / GW;
-    double2 v = src[((size_t)x0 * G + gq) * (NR * H) + c0 + w];
-    if (G > 1) {
-      const int c = c0 + w;
-      const int kp = dig_freq<NR>(c / H);
-      v = cmul(v, __ldg(pl.tw + gq * kp));
-    }
-    buf[x0 * RS + gq * W + w] = v;
+    const int gq = s / W;  // as a load slot: group gq, column w
+    s_tw[s] = __ldg(pl.tw + gq * dig_freq<NR>((c0 + w) / H));
   }
   __syncthreads();
+  // ---- diagonal tile ----
   if (pl.kind == KIND_LKR) {
+    double* coef = reinterpret_cast<double*>(buf);  // [r1][GW], aliases the data tile
     const double* U1 = pl.U + (size_t)pl.r1 * N;
     const double* U2 = pl.U + (size_t)2 * pl.r1 * N;
     for (int i = threadIdx.x; i < pl.r1 * GW; i += blockDim.x) {
       const int s = i % GW, rr = i / GW;
       coef[rr * GW + s] = __ldg(U1 + rr * N + s_k1[s]) * __ldg(U2 + rr * N + s_k2[s]);
     }
-  }
-  if (G > 1) fft_smem<G, false>(buf, N * W, GAddr<W>{RS}, pl.tw, N);
-  fft_smem<N, false>(buf, GW, X0Addr{RS}, pl.tw, N);
-
-  // diagonal scaling (+ Parseval r.z for the PCG)
-  const double scale = 2.0 / ((double)N * N * N);
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
-    const int s = i % GW, pos0 = i / GW;
-    const int k0 = dig_freq<N>(pos0);
-    const int k1 = s_k1[s], k2 = s_k2[s];
-    double D;
-    if (pl.kind == KIND_LKR) {
-      D = 0.0;
-      const double* U0 = pl.U + k0;
-      for (int rr = 0; rr < pl.r1; ++rr) D = fma(__ldg(U0 + rr * N), coef[rr * GW + s], D);
-    } else {
-      const double gsum = (__ldg(pl.lam + k0) + __ldg(pl.lam + k1)) + __ldg(pl.lam + k2);
+    __syncthreads();
+    constexpr int PQ = N / 4, SQ = GW / 2;
+    for (int i = threadIdx.x; i < PQ * SQ; i += blockDim.x) {
+      const int sq = i % SQ, pq = i / SQ;
+      double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+      const double* up = pl.Up + 4 * pq;
+      for (int rr = 0; rr < pl.r1; ++rr) {
+        const double2 ua = __ldg(reinterpret_cast<const double2*>(up + (size_t)rr * N));
+        const double2 ub = __ldg(reinterpret_cast<const double2*>(up + (size_t)rr * N) + 1);
+        const double2 cc = *reinterpret_cast<const double2*>(coef + rr * GW + 2 * sq);
+        acc[0][0] = fma(ua.x, cc.x, acc[0][0]); acc[0][1] = fma(ua.x, cc.y, acc[0][1]);
+        acc[1][0] = fma(ua.y, cc.x, acc[1][0]); acc[1][1] = fma(ua.y, cc.y, acc[1][1]);
+        acc[2][0] = fma(ub.x, cc.x, acc[2][0]); acc[2][1] = fma(ub.x, cc.y, acc[2][1]);
+        acc[3][0] = fma(ub.y, cc.x, acc[3][0]); acc[3][1] = fma(ub.y, cc.y, acc[3][1]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        Dsm[(4 * pq + a) * GW + 2 * sq] = acc[a][0];
+        Dsm[(4 * pq + a) * GW + 2 * sq + 1] = acc[a][1];
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
+      const int s = i % GW, pos0 = i / GW;
+      const int k0 = dig_freq<N>(pos0);
+      const double gsum = (__ldg(pl.lam + k0) + __ldg(pl.lam + s_k1[s])) + __ldg(pl.lam + s_k2[s]);
+      double D;
       if (pl.kind == KIND_REGULARIZED && pl.delta > 0.0) {
         D = 1.0 / (gsum + pl.delta);
       } else {
         D = (gsum > 0.0) ? 1.0 / gsum : 0.0;
       }
+      Dsm[pos0 * GW + s] = D;
     }
-    double2 v = buf[pos0 * RS + s];
-    if (MODE == MID_PCG) {
-      if ((k0 | k1 | k2) == 0) {
-        D = 0.0;  // mean projection of z (solver.py:153,179)
-      }
-      const double wgt = (k2 == 0 || k2 == N2) ? 1.0 : 2.0;
-      acc = fma(wgt * D, v.x * v.x + v.y * v.y, acc);
-    }
-    buf[pos0 * RS + s] = cscale(v, D * scale);
   }
   __syncthreads();
-  fft_smem<N, true>(buf, GW, X0Addr{RS}, pl.tw, N);
-  if (G > 1) fft_smem<G, true>(buf, N * W, GAddr<W>{RS}, pl.tw, N);
-  double2* dst = S + (size_t)b * N * G * (NR * H);
-  for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
-    const int w = i % W, gq = (i / W) % G, x0 = i / GW;
-    double2 v = buf[x0 * RS + gq * W + w];
-    if (G > 1) {
-      const int c = c0 + w;
-      const int kp = dig_freq<NR>(c / H);
-      v = cmulc(v, __ldg(pl.tw + gq * kp));
-    }
-    dst[((size_t)x0 * G + gq) * (NR * H) + c0 + w] = v;
+  if (MODE == MID_PCG && threadIdx.x < GW) {
+    // mean projection of z (solver.py:153,179): zero-frequency coefficient 0
+    // (pos0 = 0 <-> k0 = 0; slot with k1 = k2 = 0)
+    if (s_k1[threadIdx.x] == 0 && s_k2[threadIdx.x] == 0) Dsm[threadIdx.x] = 0.0;
   }
-  if (MODE == MID_PCG) {
-    double t0, t1;
-    if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
-                     scratch, t0, t1)) {
-      if (threadIdx.x == 0) {
-        const double rz = t0 / ((double)N * N * N);  // Parseval: r.z = (1/N^3) sum conj(R) D R
-        if (it == 0) {
-          st->rz[0] = rz;
-          st->norm_pf = sqrt(fabs(rz));  // solver.py:156
-          st->beta = 0.0;
-        } else {
-          st->beta = rz / st->rz[(it - 1) & 1];  // solver.py:184
-          st->rz[it & 1] = rz;
-          if (ctl.prs && sqrt(fabs(rz)) / st->norm_pf <= ctl.tol) {  // solver.py:181-183
-            st->status = ST_CONVERGED;
-            st->iters = it;
-          } else if (it >= ctl.max_iter) {
-            st->status = ST_NOT_CONVERGED;
-            st->iters = it;
+  __syncthreads();
+
+  const double scale = 2.0 / ((double)N * N * N);
+  for (int j = 0; j < NB; ++j) {
+    const int b = b0 + j;
+    if (b >= B) break;
+    RState* st = (MODE == MID_PCG) ? ctl.st + b : nullptr;
+    if (MODE == MID_PCG && st->status != ST_ACTIVE) continue;
+    double2* base = S + (size_t)b * N * G * (NR * H);
+    for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
+      const int w = i % W, gq = (i / W) % G, x0 = i / GW;
+      double2 v = base[((size_t)x0 * G + gq) * (NR * H) + c0 + w];
+      if (G > 1) v = cmul(v, s_tw[gq * W + w]);
+      buf[x0 * RS + gq * W + w] = v;
+    }
+    __syncthreads();
+    if (G > 1) fft_smem<G, false, N * W>(buf, GAddr<W>{RS}, pl.tw, N);
+    fft_smem<N, false, GW>(buf, X0Addr{RS}, pl.tw, N);
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
+      const int s = i % GW, pos0 = i / GW;
+      const double D = Dsm[pos0 * GW + s];
+      const double2 v = buf[pos0 * RS + s];
+      if (MODE == MID_PCG) {
+        const int k2 = s_k2[s];
+        const double wgt = (k2 == 0 || k2 == N2) ? 1.0 : 2.0;
+        acc = fma(wgt * D, v.x * v.x + v.y * v.y, acc);
+      }
+      buf[pos0 * RS + s] = cscale(v, D * scale);
+    }
+    __syncthreads();
+    fft_smem<N, true, GW>(buf, X0Addr{RS}, pl.tw, N);
+    if (G > 1) fft_smem<G, true, N * W>(buf, GAddr<W>{RS}, pl.tw, N);
+    for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
+      const int w = i % W, gq = (i / W) % G, x0 = i / GW;
+      double2 v = buf[x0 * RS + gq * W + w];
+      if (G > 1) v = cmulc(v, s_tw[gq * W + w]);
+      base[((size_t)x0 * G + gq) * (NR * H) + c0 + w] = v;
+    }
+    if (MODE == MID_PCG) {
+      double t0, t1;
+      if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
+                       scratch, t0, t1)) {
+        if (threadIdx.x == 0) {
+          const double rz = t0 / ((double)N * N * N);  // Parseval: r.z = (1/N^3) sum conj(R) D R
+          if (it == 0) {
+            st->rz[0] = rz;
+            st->norm_pf = sqrt(fabs(rz));  // solver.py:156
+            st->beta = 0.0;
+          } else {
+            st->beta = rz / st->rz[(it - 1) & 1];  // solver.py:184
+            st->rz[it & 1] = rz;
+            if (ctl.prs && sqrt(fabs(rz)) / st->norm_pf <= ctl.tol) {  // solver.py:181-183
+              st->status = ST_CONVERGED;
+              st->iters = it;
+            } else if (it >= ctl.max_iter) {
+              st->status = ST_NOT_CONVERGED;
+              st->iters = it;
+            }
           }
         }
       }
+    } else {
+      __syncthreads();  // buf is reloaded for the next realization
     }
   }
 }
@@ -630,10 +753,10 @@ __global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restric
   const double2* srcp = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
   for (int i = threadIdx.x; i < NR * H; i += blockDim.x) buf[i] = srcp[i];
   __syncthreads();
-  fft_smem<NR, true>(buf, H, ColAddr{HP}, pl.tw, N);
+  fft_smem<NR, true, H>(buf, ColAddr{HP}, pl.tw, N);
   c2r_pre<N>(buf, NR, HP, pl.tw);
   __syncthreads();
-  fft_smem<N2, true>(buf, NR, RowAddr{HP}, pl.tw, N);
+  fft_smem<N2, true, NR>(buf, RowAddr{HP}, pl.tw, N);
   const double* sm = reinterpret_cast<const double*>(buf);
   for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
     const int t = i / N, x2 = i - (i / N) * N;
