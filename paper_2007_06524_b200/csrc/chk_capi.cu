@@ -98,17 +98,20 @@ int fail(int code, const std::string& msg) {
 template <int N>
 struct Cfg;
 // NB realizations share one evaluation of the diagonal tile in the middle pass.
-template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8,  NB = 4; };
-template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16, NB = 4; };
-template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4; };
-template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 8; };
-template <> struct Cfg<128> { static constexpr int G = 2,  W = 8,  NB = 8; };
-template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 4; };
-template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2; };
+// REG: register-resident middle pass (first x0 radix RA in phase A, P
+// realizations in flight per CTA); otherwise the shared-memory stage kernel.
+template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8,  NB = 4, REG = 1, RA = 8, P = 4; };
+template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 2; };
+template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 2; };
+template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 8, REG = 1, RA = 8, P = 2; };
+template <> struct Cfg<128> { static constexpr int G = 2,  W = 8,  NB = 8, REG = 1, RA = 8, P = 2; };
+template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 4, REG = 0, RA = 1, P = 1; };
+template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2, REG = 0, RA = 1, P = 1; };
 
 template <int N>
 struct Ops {
   static constexpr int G = Cfg<N>::G, W = Cfg<N>::W, NB = Cfg<N>::NB, NR = N / G, H = N / 2 + 1;
+  static constexpr int REG = Cfg<N>::REG, RA = Cfg<N>::RA, P = Cfg<N>::P;
   static constexpr int TILES = NR * H / W;
   static constexpr int PLANE_BLOCKS = N * G;  // per realization
   static constexpr size_t plane_smem() { return (size_t)NR * H * sizeof(double2); }
@@ -144,10 +147,18 @@ struct Ops {
   }
   template <int NBX, int MODE>
   static int mid_launch(cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it) {
-    const size_t sm = mid_smem(pl.kind == KIND_LKR ? pl.r1 : 0);
+    const int r1 = pl.kind == KIND_LKR ? pl.r1 : 0;
     dim3 grid(((B + NBX - 1) / NBX) * TILES), block(256);
-    CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, NBX, MODE>, sm));
-    mid_column_kernel<N, G, W, NBX, MODE><<<grid, block, sm, s>>>(S, pl, ctl, it, B);
+    if constexpr (REG) {
+      constexpr int PX = (NBX == 1) ? 1 : P;
+      const size_t sm = (size_t)mid_dsm_offset(PX * N * (G * W + 1), G * W, r1) + (size_t)N * G * W * sizeof(double);
+      CHK_CUDA(allow_smem(mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE>, sm));
+      mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE><<<grid, block, sm, s>>>(S, pl, ctl, it, B);
+    } else {
+      const size_t sm = mid_smem(r1);
+      CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, NBX, MODE>, sm));
+      mid_column_kernel<N, G, W, NBX, MODE><<<grid, block, sm, s>>>(S, pl, ctl, it, B);
+    }
     return CHK_OK;
   }
   static int mid(int mode, cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it) {

@@ -20,6 +20,7 @@
 // them in a fixed order and takes the scalar decisions (alpha, beta, stop).
 #pragma once
 #include "chk_fft.cuh"
+#include "chk_tma.cuh"
 
 namespace chk {
 
@@ -399,7 +400,7 @@ __device__ __forceinline__ void c2r_pre(double2* buf, int nrows, int hp,
 // kernel 1: pq = <p, A p>  (solver.py:162-165)
 // ----------------------------------------------------------------------------
 template <int N, int G>
-__global__ void __launch_bounds__(256) stencil_dot_kernel(Geo g, const double* __restrict__ beta,
+__global__ void __launch_bounds__(256, 3) stencil_dot_kernel(Geo g, const double* __restrict__ beta,
                                                           const double* __restrict__ p,
                                                           SolveCtl ctl, int it) {
   constexpr int NR = N / G;
@@ -547,8 +548,15 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
   __syncthreads();
   // C2C along the x1 group (length NR)
   fft_smem<NR, false, H>(buf, ColAddr{HP}, pl.tw, N);
+  // the slab is contiguous in smem (HP == H) and in HBM: one bulk store
   double2* dst = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
-  for (int i = threadIdx.x; i < NR * H; i += blockDim.x) dst[i] = buf[i];
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bulk_s2g(dst, buf, (uint32_t)(NR * H * sizeof(double2)));
+    bulk_commit();
+    bulk_wait_read0();
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -727,6 +735,305 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
 }
 
 // ----------------------------------------------------------------------------
+// ----------------------------------------------------------------------------
+// kernel 3b: register-resident spectral column pass (n <= 128)
+// ----------------------------------------------------------------------------
+// In-register in-place DIF / inverse DIT of length L on v[0..L): identical
+// index semantics to fft_smem<L> (digit-reversed output), all loops unrolled.
+template <int L, int M, bool INV>
+struct RegFft {
+  __device__ __forceinline__ static void run(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
+    constexpr int R = Radix<M>::value, S = M / R;
+    if constexpr (INV && S > 1) RegFft<L, S, true>::run(v, tw, ntab);
+#pragma unroll
+    for (int blk = 0; blk < L / M; ++blk) {
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        double2 a[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) a[t] = v[blk * M + j + t * S];
+        if constexpr (!INV) {
+          dftR<R, false>(a);
+          if (j > 0) {
+#pragma unroll
+            for (int m = 1; m < R; ++m) a[m] = cmul(a[m], __ldg(tw + (j * m) * (ntab / M)));
+          }
+        } else {
+          if (j > 0) {
+#pragma unroll
+            for (int m = 1; m < R; ++m) a[m] = cmulc(a[m], __ldg(tw + (j * m) * (ntab / M)));
+          }
+          dftR<R, true>(a);
+        }
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[blk * M + j + t * S] = a[t];
+      }
+    }
+    if constexpr (!INV && S > 1) RegFft<L, S, false>::run(v, tw, ntab);
+  }
+};
+template <int L, bool INV>
+__device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
+  if constexpr (L > 1) RegFft<L, L, INV>::run(v, tw, ntab);
+}
+
+// Phase A (thread = column w, x0 offset j): the G-group combine and the first
+// radix-RA x0 stage straight from/to global memory in registers; phase B
+// (thread = slot s, block of RB = N/RA positions): the remaining x0 stages,
+// the diagonal scaling and the inverse stages in registers.  Shared memory is
+// touched twice per element per direction (one exchange each way).  P
+// realizations are in flight per CTA; NB share one diagonal tile.
+template <int N, int G, int W, int RA, int NB, int P, int MODE>
+__global__ void __launch_bounds__(256, 2) mid_column_reg_kernel(double2* __restrict__ S, PlanDev pl,
+                                                             SolveCtl ctl, int it, int B) {
+  constexpr int NR = N / G;
+  constexpr int N2 = N / 2;
+  constexpr int H = N2 + 1;
+  constexpr int TILES = NR * H / W;
+  constexpr int GW = G * W;
+  constexpr int RS = GW + 1;
+  constexpr int RB = N / RA;      // positions per phase-B block
+  constexpr int JA = N / RA;      // x0 stride of a phase-A butterfly
+  constexpr int ITEMS_A = W * JA;
+  constexpr int ITEMS_B = GW * RA;
+  static_assert(NB % P == 0, "NB must be a multiple of P");
+  static_assert(RA == Radix<N>::value, "phase A must be the first stage of fft_smem<N> (dig_freq order)");
+  extern __shared__ double2 buf[];  // [P][N][RS] (aliased by the [r1][GW] coefficients)
+  const int doff = mid_dsm_offset(P * N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
+  double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
+  __shared__ double scratch[32];
+  __shared__ int s_k1[GW], s_k2[GW];
+  __shared__ double s_wgt[GW];
+  __shared__ double2 s_tw[GW];
+  __shared__ int s_act[NB];
+  const int bg = blockIdx.x / TILES;
+  const int tile = blockIdx.x - bg * TILES;
+  const int c0 = tile * W;
+  const int b0 = bg * NB;
+
+  if (threadIdx.x == 0) {
+    int any = 0;
+    for (int j = 0; j < NB; ++j) {
+      const int b = b0 + j;
+      int a = (b < B);
+      if (a && MODE == MID_PCG) a = (ctl.st[b].status == ST_ACTIVE);
+      s_act[j] = a;
+      any |= a;
+    }
+    scratch[0] = any;
+  }
+  __syncthreads();
+  if (scratch[0] == 0.0) return;
+  for (int s = threadIdx.x; s < GW; s += blockDim.x) {
+    const int m = dig_freq<G>(s / W), w = s % W;
+    const int c = c0 + w;
+    const int q1 = c / H, q2 = c - (c / H) * H;
+    const int kp = dig_freq<NR>(q1);
+    s_k1[s] = kp + m * NR;
+    const int k2 = (q2 == N2) ? N2 : dig_freq<N2>(q2);
+    s_k2[s] = k2;
+    s_wgt[s] = (k2 == 0 || k2 == N2) ? 1.0 : 2.0;
+    s_tw[s] = __ldg(pl.tw + (s / W) * kp);  // as a load slot (group s/W, column w)
+  }
+  __syncthreads();
+  // ---- diagonal tile (once per CTA) ----
+  if (pl.kind == KIND_LKR) {
+    double* coef = reinterpret_cast<double*>(buf);
+    const double* U1 = pl.U + (size_t)pl.r1 * N;
+    const double* U2 = pl.U + (size_t)2 * pl.r1 * N;
+    for (int i = threadIdx.x; i < pl.r1 * GW; i += blockDim.x) {
+      const int s = i % GW, rr = i / GW;
+      coef[rr * GW + s] = __ldg(U1 + rr * N + s_k1[s]) * __ldg(U2 + rr * N + s_k2[s]);
+    }
+    __syncthreads();
+    constexpr int PQ = N / 4, SQ = GW / 2;
+    for (int i = threadIdx.x; i < PQ * SQ; i += blockDim.x) {
+      const int sq = i % SQ, pq = i / SQ;
+      double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+      const double* up = pl.Up + 4 * pq;
+      for (int rr = 0; rr < pl.r1; ++rr) {
+        const double2 ua = __ldg(reinterpret_cast<const double2*>(up + (size_t)rr * N));
+        const double2 ub = __ldg(reinterpret_cast<const double2*>(up + (size_t)rr * N) + 1);
+        const double2 cc = *reinterpret_cast<const double2*>(coef + rr * GW + 2 * sq);
+        acc[0][0] = fma(ua.x, cc.x, acc[0][0]); acc[0][1] = fma(ua.x, cc.y, acc[0][1]);
+        acc[1][0] = fma(ua.y, cc.x, acc[1][0]); acc[1][1] = fma(ua.y, cc.y, acc[1][1]);
+        acc[2][0] = fma(ub.x, cc.x, acc[2][0]); acc[2][1] = fma(ub.x, cc.y, acc[2][1]);
+        acc[3][0] = fma(ub.y, cc.x, acc[3][0]); acc[3][1] = fma(ub.y, cc.y, acc[3][1]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        Dsm[(4 * pq + a) * GW + 2 * sq] = acc[a][0];
+        Dsm[(4 * pq + a) * GW + 2 * sq + 1] = acc[a][1];
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
+      const int s = i % GW, pos0 = i / GW;
+      const int k0 = dig_freq<N>(pos0);
+      const double gsum = (__ldg(pl.lam + k0) + __ldg(pl.lam + s_k1[s])) + __ldg(pl.lam + s_k2[s]);
+      double D;
+      if (pl.kind == KIND_REGULARIZED && pl.delta > 0.0) {
+        D = 1.0 / (gsum + pl.delta);
+      } else {
+        D = (gsum > 0.0) ? 1.0 / gsum : 0.0;
+      }
+      Dsm[pos0 * GW + s] = D;
+    }
+  }
+  __syncthreads();
+  if (MODE == MID_PCG && threadIdx.x < GW) {
+    if (s_k1[threadIdx.x] == 0 && s_k2[threadIdx.x] == 0) Dsm[threadIdx.x] = 0.0;  // mean projection
+  }
+  __syncthreads();
+
+  const double scale = 2.0 / ((double)N * N * N);
+  const int ntab = N;
+  for (int c = 0; c < NB / P; ++c) {
+    // ---- phase A forward: global -> registers -> smem ----
+    for (int item = threadIdx.x; item < P * ITEMS_A; item += blockDim.x) {
+      const int pr = item / ITEMS_A, ia = item - pr * ITEMS_A;
+      if (!s_act[c * P + pr]) continue;
+      const int w = ia % W, j = ia / W;
+      const double2* base = S + (size_t)(b0 + c * P + pr) * N * G * (NR * H) + c0 + w;
+      double2 v[G][RA];
+#pragma unroll
+      for (int t = 0; t < RA; ++t)
+#pragma unroll
+        for (int g = 0; g < G; ++g) v[g][t] = base[((size_t)(j + JA * t) * G + g) * (NR * H)];
+      if constexpr (G > 1) {
+#pragma unroll
+        for (int g = 1; g < G; ++g) {
+          const double2 tg = s_tw[g * W + w];
+#pragma unroll
+          for (int t = 0; t < RA; ++t) v[g][t] = cmul(v[g][t], tg);
+        }
+#pragma unroll
+        for (int t = 0; t < RA; ++t) {
+          double2 a[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) a[g] = v[g][t];
+          reg_fft<G, false>(a, pl.tw, ntab);
+#pragma unroll
+          for (int g = 0; g < G; ++g) v[g][t] = a[g];
+        }
+      }
+      double2* dst = buf + pr * N * RS;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        dftR<RA, false>(v[g]);
+#pragma unroll
+        for (int m = 0; m < RA; ++m) {
+          double2 y = v[g][m];
+          if (m > 0 && j > 0) y = cmul(y, __ldg(pl.tw + (j * m) * (ntab / N)));
+          dst[(j + JA * m) * RS + g * W + w] = y;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase B: remaining stages, diagonal, inverse (registers) ----
+    double acc[P];
+#pragma unroll
+    for (int pr = 0; pr < P; ++pr) acc[pr] = 0.0;
+    for (int item = threadIdx.x; item < P * ITEMS_B; item += blockDim.x) {
+      const int pr = item / ITEMS_B, ib = item - pr * ITEMS_B;
+      if (!s_act[c * P + pr]) continue;
+      const int s = ib % GW, blk = ib / GW;
+      double2* row = buf + pr * N * RS + (blk * RB) * RS + s;
+      double2 v[RB];
+#pragma unroll
+      for (int e = 0; e < RB; ++e) v[e] = row[e * RS];
+      reg_fft<RB, false>(v, pl.tw, ntab);
+      double a = 0.0;
+      const double wgt = s_wgt[s];
+#pragma unroll
+      for (int e = 0; e < RB; ++e) {
+        const double D = Dsm[(blk * RB + e) * GW + s];
+        if (MODE == MID_PCG) a = fma(wgt * D, v[e].x * v[e].x + v[e].y * v[e].y, a);
+        v[e] = cscale(v[e], D * scale);
+      }
+#pragma unroll
+      for (int pr2 = 0; pr2 < P; ++pr2)
+        if (pr2 == pr) acc[pr2] += a;
+      reg_fft<RB, true>(v, pl.tw, ntab);
+#pragma unroll
+      for (int e = 0; e < RB; ++e) row[e * RS] = v[e];
+    }
+    __syncthreads();
+    // ---- phase A inverse: smem -> registers -> global ----
+    for (int item = threadIdx.x; item < P * ITEMS_A; item += blockDim.x) {
+      const int pr = item / ITEMS_A, ia = item - pr * ITEMS_A;
+      if (!s_act[c * P + pr]) continue;
+      const int w = ia % W, j = ia / W;
+      const double2* src = buf + pr * N * RS;
+      double2 v[G][RA];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int m = 0; m < RA; ++m) {
+          double2 y = src[(j + JA * m) * RS + g * W + w];
+          if (m > 0 && j > 0) y = cmulc(y, __ldg(pl.tw + (j * m) * (ntab / N)));
+          v[g][m] = y;
+        }
+        dftR<RA, true>(v[g]);
+      }
+      if constexpr (G > 1) {
+#pragma unroll
+        for (int t = 0; t < RA; ++t) {
+          double2 a[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) a[g] = v[g][t];
+          reg_fft<G, true>(a, pl.tw, ntab);
+#pragma unroll
+          for (int g = 0; g < G; ++g) v[g][t] = a[g];
+        }
+#pragma unroll
+        for (int g = 1; g < G; ++g) {
+          const double2 tg = s_tw[g * W + w];
+#pragma unroll
+          for (int t = 0; t < RA; ++t) v[g][t] = cmulc(v[g][t], tg);
+        }
+      }
+      double2* base = S + (size_t)(b0 + c * P + pr) * N * G * (NR * H) + c0 + w;
+#pragma unroll
+      for (int t = 0; t < RA; ++t)
+#pragma unroll
+        for (int g = 0; g < G; ++g) base[((size_t)(j + JA * t) * G + g) * (NR * H)] = v[g][t];
+    }
+    // ---- per-realization Parseval reductions ----
+    if (MODE == MID_PCG) {
+#pragma unroll
+      for (int pr = 0; pr < P; ++pr) {
+        const int b = b0 + c * P + pr;
+        if (!s_act[c * P + pr]) continue;
+        RState* st = ctl.st + b;
+        double t0, t1;
+        if (reduce2_last(acc[pr], 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
+                         scratch, t0, t1)) {
+          if (threadIdx.x == 0) {
+            const double rz = t0 / ((double)N * N * N);
+            if (it == 0) {
+              st->rz[0] = rz;
+              st->norm_pf = sqrt(fabs(rz));
+              st->beta = 0.0;
+            } else {
+              st->beta = rz / st->rz[(it - 1) & 1];
+              st->rz[it & 1] = rz;
+              if (ctl.prs && sqrt(fabs(rz)) / st->norm_pf <= ctl.tol) {
+                st->status = ST_CONVERGED;
+                st->iters = it;
+              } else if (it >= ctl.max_iter) {
+                st->status = ST_NOT_CONVERGED;
+                st->iters = it;
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // kernel 4: inverse plane transform + direction update
 // ----------------------------------------------------------------------------
 enum : int { INV_APPLY = 0, INV_PCG = 1 };
@@ -751,8 +1058,18 @@ __global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restric
     beta = st->beta;
   }
   const double2* srcp = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
-  for (int i = threadIdx.x; i < NR * H; i += blockDim.x) buf[i] = srcp[i];
-  __syncthreads();
+  __shared__ alignas(8) uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_arrive_expect_tx(&bar, (uint32_t)(NR * H * sizeof(double2)));
+    bulk_g2s(buf, srcp, (uint32_t)(NR * H * sizeof(double2)), &bar);
+  }
+  if (MODE == INV_PCG && it > 0 && threadIdx.x < NR) {
+    // p rows of this slab are read after the transforms: warm L2 now
+    bulk_prefetch_l2(out + b * nb + ((size_t)x0 * N + gg + G * threadIdx.x) * N, N * sizeof(double));
+  }
+  __syncthreads();  // barrier initialised before anyone waits
+  mbar_wait(&bar, 0);
   fft_smem<NR, true, H>(buf, ColAddr{HP}, pl.tw, N);
   c2r_pre<N>(buf, NR, HP, pl.tw);
   __syncthreads();
