@@ -100,13 +100,16 @@ struct Cfg;
 // NB realizations share one evaluation of the diagonal tile in the middle pass.
 // REG: register-resident middle pass (first x0 radix RA in phase A, P
 // realizations in flight per CTA); otherwise the shared-memory stage kernel.
-template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8,  NB = 4, REG = 1, RA = 8, P = 4; };
-template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 2; };
-template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 2; };
-template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 8, REG = 1, RA = 8, P = 2; };
-template <> struct Cfg<128> { static constexpr int G = 2,  W = 8,  NB = 8, REG = 1, RA = 8, P = 2; };
+template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8,  NB = 4, REG = 1, RA = 8, P = 1; };
+template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 1; };
+template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 1; };
+template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 8, REG = 1, RA = 8, P = 1; };
+template <> struct Cfg<128> { static constexpr int G = 2,  W = 8,  NB = 8, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 4, REG = 0, RA = 1, P = 1; };
 template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2, REG = 0, RA = 1, P = 1; };
+
+// every h-cell inside its sub-cell (alpha = 1/2): stencil fast path
+inline bool allin(const Geo& g) { return g.k == g.mask + 1 && g.off == 0; }
 
 template <int N>
 struct Ops {
@@ -133,14 +136,17 @@ struct Ops {
     dim3 grid(B * PLANE_BLOCKS), block(256);
     ProfScope ps(1, s);
     if (mode == FWD_APPLY) {
-      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_APPLY>, sm));
-      fwd_plane_kernel<N, G, FWD_APPLY><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_APPLY, false>, sm));
+      fwd_plane_kernel<N, G, FWD_APPLY, false><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
     } else if (mode == FWD_INIT) {
-      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_INIT>, sm));
-      fwd_plane_kernel<N, G, FWD_INIT><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_INIT, false>, sm));
+      fwd_plane_kernel<N, G, FWD_INIT, false><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+    } else if (allin(g)) {
+      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_ITER, true>, sm));
+      fwd_plane_kernel<N, G, FWD_ITER, true><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
     } else {
-      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_ITER>, sm));
-      fwd_plane_kernel<N, G, FWD_ITER><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_ITER, false>, sm));
+      fwd_plane_kernel<N, G, FWD_ITER, false><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
     }
     CHK_LAUNCHED();
     return CHK_OK;
@@ -151,9 +157,10 @@ struct Ops {
     dim3 grid(((B + NBX - 1) / NBX) * TILES), block(256);
     if constexpr (REG) {
       constexpr int PX = (NBX == 1) ? 1 : P;
+      constexpr int NT = 128 * PX;
       const size_t sm = (size_t)mid_dsm_offset(PX * N * (G * W + 1), G * W, r1) + (size_t)N * G * W * sizeof(double);
-      CHK_CUDA(allow_smem(mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE>, sm));
-      mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE><<<grid, block, sm, s>>>(S, pl, ctl, it, B);
+      CHK_CUDA(allow_smem(mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT>, sm));
+      mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT><<<grid, NT, sm, s>>>(S, pl, ctl, it, B);
     } else {
       const size_t sm = mid_smem(r1);
       CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, NBX, MODE>, sm));
@@ -192,13 +199,19 @@ struct Ops {
   static int dot(cudaStream_t s, int B, Geo g, const double* beta, const double* p, SolveCtl ctl,
                  int it) {
     ProfScope ps(0, s);
-    stencil_dot_kernel<N, G><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, p, ctl, it);
+    if (allin(g))
+      stencil_dot_kernel<N, G, true><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, p, ctl, it);
+    else
+      stencil_dot_kernel<N, G, false><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, p, ctl, it);
     CHK_LAUNCHED();
     return CHK_OK;
   }
   static int stencil(cudaStream_t s, int B, Geo g, const double* beta, const double* x, double* y,
                      double* xy, double* part, unsigned* cnt) {
-    stencil_apply_kernel<N, G><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, x, y, xy, part, cnt);
+    if (allin(g))
+      stencil_apply_kernel<N, G, true><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, x, y, xy, part, cnt);
+    else
+      stencil_apply_kernel<N, G, false><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, x, y, xy, part, cnt);
     CHK_LAUNCHED();
     return CHK_OK;
   }

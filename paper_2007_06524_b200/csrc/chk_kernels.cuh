@@ -248,8 +248,78 @@ __device__ __forceinline__ void stencil4(const Geo& g, const RowCtx& rc, int x2s
   }
 }
 
+// Fast path when every h-cell lies inside its sub-cell (k == n0, offset 0, i.e.
+// alpha = 1/2, the BASELINE configurations): F = beta(cell) everywhere, the
+// quad x2s..x2s+3 shares one cell column, and nodes 1..3 of the quad share
+// their six edge weights.  Same formulas and summation order as stencil4.
+__device__ __forceinline__ void stencil4_allin(const Geo& g, const double* __restrict__ p,
+                                               const double* __restrict__ beta, int x0, int x1,
+                                               int x2s, double (&pc)[4], double (&q)[4]) {
+  const int n = g.n, nm = n - 1;
+  const long long nn = (long long)n * n;
+  const long long row = (long long)x0 * nn + (long long)x1 * n;
+  const long long d0m = (x0 == 0) ? (long long)nm * nn : -nn;
+  const long long d0p = (x0 == nm) ? -(long long)nm * nn : nn;
+  const long long d1m = (x1 == 0) ? (long long)nm * n : -(long long)n;
+  const long long d1p = (x1 == nm) ? -(long long)nm * n : (long long)n;
+  const double* pr = p + row + x2s;
+  double xm[4], xp[4], ym[4], yp[4];
+  ld4(pr, pc);
+  ld4(pr + d0m, xm);
+  ld4(pr + d0p, xp);
+  ld4(pr + d1m, ym);
+  ld4(pr + d1p, yp);
+  const double pl = __ldg(p + row + ((x2s - 1) & nm));
+  const double prr = __ldg(p + row + ((x2s + 4) & nm));
+  // cell rows (c(j0), c(j1), :) for j0 in {x0-1, x0}, j1 in {x1-1, x1}
+  const int L = g.L, sh = g.sh;
+  const int c0m = ((x0 - 1) & nm) >> sh, c00 = x0 >> sh;
+  const int c1m = ((x1 - 1) & nm) >> sh, c10 = x1 >> sh;
+  const int cm = ((x2s - 1) & nm) >> sh, cc = x2s >> sh;
+  const double* b00 = beta + ((size_t)c0m * L + c1m) * L;  // (x0-1, x1-1)
+  const double* b01 = beta + ((size_t)c0m * L + c10) * L;  // (x0-1, x1)
+  const double* b10 = beta + ((size_t)c00 * L + c1m) * L;  // (x0,   x1-1)
+  const double* b11 = beta + ((size_t)c00 * L + c10) * L;  // (x0,   x1)
+  const double m00 = __ldg(b00 + cm), m01 = __ldg(b01 + cm), m10 = __ldg(b10 + cm), m11 = __ldg(b11 + cm);
+  const double z00 = __ldg(b00 + cc), z01 = __ldg(b01 + cc), z10 = __ldg(b10 + cc), z11 = __ldg(b11 + cc);
+  const double lam = g.lam;
+  auto wsum = [lam](double a, double b, double c, double d) { return lam + (((a + b) + c) + d) * 0.25; };
+  // node 0: h-cells x2-1 -> m.., x2 -> z..
+  const double A0p = wsum(z11, m11, z10, m10), A0m = wsum(z01, m01, z00, m00);
+  const double A1p = wsum(z11, m11, z01, m01), A1m = wsum(z10, m10, z00, m00);
+  const double A2p = wsum(z11, z10, z01, z00), A2m = wsum(m11, m10, m01, m00);
+  // nodes 1..3: both h-cells in the quad's cell
+  const double B0p = wsum(z11, z11, z10, z10), B0m = wsum(z01, z01, z00, z00);
+  const double B1p = wsum(z11, z11, z01, z01), B1m = wsum(z10, z10, z00, z00);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double g0p = i ? B0p : A0p, g0m = i ? B0m : A0m;
+    const double g1p = i ? B1p : A1p, g1m = i ? B1m : A1m;
+    const double g2p = A2p, g2m = i ? A2p : A2m;
+    const double c = pc[i];
+    const double left = (i == 0) ? pl : pc[i - 1];
+    const double right = (i == 3) ? prr : pc[i + 1];
+    const double q0 = g0p * (c - xp[i]) + g0m * (c - xm[i]);
+    const double q1 = g1p * (c - yp[i]) + g1m * (c - ym[i]);
+    const double q2 = g2p * (c - right) + g2m * (c - left);
+    q[i] = (q0 + q1) + q2;
+  }
+}
+
+template <bool ALLIN>
+__device__ __forceinline__ void stencil_quad(const Geo& g, const double* __restrict__ p,
+                                             const double* __restrict__ beta, int x0, int x1,
+                                             int x2s, double (&pc)[4], double (&q)[4]) {
+  if constexpr (ALLIN) {
+    stencil4_allin(g, p, beta, x0, x1, x2s, pc, q);
+  } else {
+    const RowCtx rc = make_row(p, beta, g, x0, x1);
+    stencil4(g, rc, x2s, pc, q);
+  }
+}
+
 // Standalone matvec y = A x (+ optional <x, y>), CTA per (realization, x0, group).
-template <int N, int G>
+template <int N, int G, bool ALLIN>
 __global__ void __launch_bounds__(256) stencil_apply_kernel(Geo g, const double* __restrict__ beta,
                                                             const double* __restrict__ x,
                                                             double* __restrict__ y, double* xy,
@@ -267,9 +337,8 @@ __global__ void __launch_bounds__(256) stencil_apply_kernel(Geo g, const double*
   for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
     const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
     const int x1 = gg + G * t;
-    const RowCtx rc = make_row(xb, bb, g, x0, x1);
     double pc[4], q[4];
-    stencil4(g, rc, x2, pc, q);
+    stencil_quad<ALLIN>(g, xb, bb, x0, x1, x2, pc, q);
     double2* yo = reinterpret_cast<double2*>(y + b * nb + ((size_t)x0 * N + x1) * N + x2);
     yo[0] = make_double2(q[0], q[1]);
     yo[1] = make_double2(q[2], q[3]);
@@ -399,7 +468,7 @@ __device__ __forceinline__ void c2r_pre(double2* buf, int nrows, int hp,
 // ----------------------------------------------------------------------------
 // kernel 1: pq = <p, A p>  (solver.py:162-165)
 // ----------------------------------------------------------------------------
-template <int N, int G>
+template <int N, int G, bool ALLIN>
 __global__ void __launch_bounds__(256, 3) stencil_dot_kernel(Geo g, const double* __restrict__ beta,
                                                           const double* __restrict__ p,
                                                           SolveCtl ctl, int it) {
@@ -417,9 +486,8 @@ __global__ void __launch_bounds__(256, 3) stencil_dot_kernel(Geo g, const double
   constexpr int Q4 = N / 4;
   for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
     const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
-    const RowCtx rc = make_row(pb, bb, g, x0, gg + G * t);
     double pc[4], q[4];
-    stencil4(g, rc, x2, pc, q);
+    stencil_quad<ALLIN>(g, pb, bb, x0, gg + G * t, x2, pc, q);
     acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
   }
   double t0, t1;
@@ -440,7 +508,7 @@ __global__ void __launch_bounds__(256, 3) stencil_dot_kernel(Geo g, const double
 // ----------------------------------------------------------------------------
 enum : int { FWD_APPLY = 0, FWD_INIT = 1, FWD_ITER = 2 };
 
-template <int N, int G, int MODE>
+template <int N, int G, int MODE, bool ALLIN>
 __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __restrict__ beta,
                                                         const double* __restrict__ src,  // x (APPLY) / f (INIT) / p (ITER)
                                                         double* __restrict__ u, double* __restrict__ r,
@@ -501,9 +569,8 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
       const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
       const int x1 = gg + G * t;
       const size_t idx = b * nb + ((size_t)x0 * N + x1) * N + x2;
-      const RowCtx rc = make_row(pb, bb, g, x0, x1);
       double pc[4], q[4];
-      stencil4(g, rc, x2, pc, q);
+      stencil_quad<ALLIN>(g, pb, bb, x0, x1, x2, pc, q);
       double2* u2 = reinterpret_cast<double2*>(u + idx);
       double2* r2 = reinterpret_cast<double2*>(r + idx);
       double2 ua = u2[0], ub = u2[1], ra = r2[0], rb = r2[1];
@@ -783,8 +850,8 @@ __device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restri
 // the diagonal scaling and the inverse stages in registers.  Shared memory is
 // touched twice per element per direction (one exchange each way).  P
 // realizations are in flight per CTA; NB share one diagonal tile.
-template <int N, int G, int W, int RA, int NB, int P, int MODE>
-__global__ void __launch_bounds__(256, 2) mid_column_reg_kernel(double2* __restrict__ S, PlanDev pl,
+template <int N, int G, int W, int RA, int NB, int P, int MODE, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* __restrict__ S, PlanDev pl,
                                                              SolveCtl ctl, int it, int B) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
