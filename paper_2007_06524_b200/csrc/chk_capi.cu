@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -131,22 +132,22 @@ struct Ops {
   }
 
   static int fwd(int mode, cudaStream_t s, int B, Geo g, const double* beta, const double* src,
-                 double* u, double* r, double2* S, PlanDev pl, SolveCtl ctl, int it) {
+                 double* u, double2* S, PlanDev pl, SolveCtl ctl, int it) {
     const size_t sm = plane_smem();
     dim3 grid(B * PLANE_BLOCKS), block(256);
     ProfScope ps(1, s);
     if (mode == FWD_APPLY) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_APPLY, false>, sm));
-      fwd_plane_kernel<N, G, FWD_APPLY, false><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+      fwd_plane_kernel<N, G, FWD_APPLY, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, it);
     } else if (mode == FWD_INIT) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_INIT, false>, sm));
-      fwd_plane_kernel<N, G, FWD_INIT, false><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+      fwd_plane_kernel<N, G, FWD_INIT, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, it);
     } else if (allin(g)) {
-      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_ITER, true>, sm));
-      fwd_plane_kernel<N, G, FWD_ITER, true><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_Q, true>, sm));
+      fwd_plane_kernel<N, G, FWD_Q, true><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, it);
     } else {
-      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_ITER, false>, sm));
-      fwd_plane_kernel<N, G, FWD_ITER, false><<<grid, block, sm, s>>>(g, beta, src, u, r, S, pl, ctl, it);
+      CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_Q, false>, sm));
+      fwd_plane_kernel<N, G, FWD_Q, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, it);
     }
     CHK_LAUNCHED();
     return CHK_OK;
@@ -175,34 +176,29 @@ struct Ops {
     int rc;
     if (mode == MID_APPLY)
       rc = wide ? mid_launch<NB, MID_APPLY>(s, B, S, pl, ctl, it) : mid_launch<1, MID_APPLY>(s, B, S, pl, ctl, it);
+    else if (mode == MID_INIT)
+      rc = wide ? mid_launch<NB, MID_INIT>(s, B, S, pl, ctl, it) : mid_launch<1, MID_INIT>(s, B, S, pl, ctl, it);
     else
-      rc = wide ? mid_launch<NB, MID_PCG>(s, B, S, pl, ctl, it) : mid_launch<1, MID_PCG>(s, B, S, pl, ctl, it);
+      rc = wide ? mid_launch<NB, MID_ITER>(s, B, S, pl, ctl, it) : mid_launch<1, MID_ITER>(s, B, S, pl, ctl, it);
     if (rc) return rc;
     CHK_LAUNCHED();
     return CHK_OK;
   }
-  static int inv(int mode, cudaStream_t s, int B, const double2* S, double* out, PlanDev pl,
-                 SolveCtl ctl, int it) {
+  static int inv(int mode, cudaStream_t s, int B, const double2* S, double* out, double* u,
+                 PlanDev pl, SolveCtl ctl, int it) {
     const size_t sm = plane_smem();
     dim3 grid(B * PLANE_BLOCKS), block(256);
     ProfScope ps(3, s);
     if (mode == INV_APPLY) {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_APPLY>, sm));
-      inv_plane_kernel<N, G, INV_APPLY><<<grid, block, sm, s>>>(S, out, pl, ctl, it);
+      inv_plane_kernel<N, G, INV_APPLY><<<grid, block, sm, s>>>(S, out, u, pl, ctl, it);
+    } else if (mode == INV_INIT) {
+      CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_INIT>, sm));
+      inv_plane_kernel<N, G, INV_INIT><<<grid, block, sm, s>>>(S, out, u, pl, ctl, it);
     } else {
-      CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_PCG>, sm));
-      inv_plane_kernel<N, G, INV_PCG><<<grid, block, sm, s>>>(S, out, pl, ctl, it);
+      CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_ITER>, sm));
+      inv_plane_kernel<N, G, INV_ITER><<<grid, block, sm, s>>>(S, out, u, pl, ctl, it);
     }
-    CHK_LAUNCHED();
-    return CHK_OK;
-  }
-  static int dot(cudaStream_t s, int B, Geo g, const double* beta, const double* p, SolveCtl ctl,
-                 int it) {
-    ProfScope ps(0, s);
-    if (allin(g))
-      stencil_dot_kernel<N, G, true><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, p, ctl, it);
-    else
-      stencil_dot_kernel<N, G, false><<<B * PLANE_BLOCKS, 256, 0, s>>>(g, beta, p, ctl, it);
     CHK_LAUNCHED();
     return CHK_OK;
   }
@@ -280,7 +276,7 @@ size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Workspace {
   double* p;
-  double* r;
+  double2* Rh;
   double2* S;
   double* part;
   RState* st;
@@ -295,7 +291,7 @@ Workspace carve(void* base, int n, int B, int max_iter) {
   Workspace w{};
   size_t off = 0;
   w.p = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * nb * B);
-  w.r = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * nb * B);
+  w.Rh = reinterpret_cast<double2*>(c + off); off = align_up(off + sizeof(double2) * spec * B);
   w.S = reinterpret_cast<double2*>(c + off); off = align_up(off + sizeof(double2) * spec * B);
   w.part = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * 2 * (size_t)maxblk_of(n) * B);
   w.st = reinterpret_cast<RState*>(c + off); off = align_up(off + sizeof(RState) * B);
@@ -463,11 +459,11 @@ int32_t chk_precond_apply(const chk_precond_plan* p, const double* r, double* z,
   g.n = p->n;
   int rc = CHK_OK;
   CHK_DISPATCH(p->n, {
-    rc = O::fwd(FWD_APPLY, s, B, g, nullptr, r, nullptr, nullptr, S, pl, ctl, 0);
+    rc = O::fwd(FWD_APPLY, s, B, g, nullptr, r, nullptr, S, pl, ctl, 0);
     if (rc) return rc;
     rc = O::mid(MID_APPLY, s, B, S, pl, ctl, 0);
     if (rc) return rc;
-    rc = O::inv(INV_APPLY, s, B, S, z, pl, ctl, 0);
+    rc = O::inv(INV_APPLY, s, B, S, z, nullptr, pl, ctl, 0);
   });
   return rc;
 }
@@ -528,8 +524,9 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
   if (!workspace || workspace_bytes < w.bytes) return fail(CHK_EINVAL, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PlanDev pl = plan_dev(plan);
-  SolveCtl ctl{w.st, w.part, w.hist, maxblk_of(n), opts->max_iter, opts->tol,
-               opts->precond_residual_stopping ? 1 : 0};
+  SolveCtl ctl{w.st, w.Rh, w.part, w.hist, maxblk_of(n), opts->max_iter, opts->tol,
+               opts->precond_residual_stopping ? 1 : 0, 0};
+  if (const char* dbg = getenv("CHK_DEBUG_FLAGS")) ctl.dbg = atoi(dbg);
   RState* hst_all = g_pinned.get((size_t)2 * B);
   RState* hst = hst_all;
   if (!hst_all) return fail(CHK_ECUDA, "cudaMallocHost failed");
@@ -542,20 +539,23 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
   auto run = [&]() -> int {
     int rc2 = CHK_OK;
     CHK_DISPATCH(n, {
-      // initialisation: r = f (projected), u = 0, z = P r, p = z  (solver.py:131-156)
+      // initialisation: r = f (projected), u = 0, z = P r, p = z  (solver.py:131-156);
+      // r is kept as its spectrum R from here on
       if ((rc2 = O::rhs_stats(s, B, f, ctl))) return rc2;
-      if ((rc2 = O::fwd(FWD_INIT, s, B, g, beta, f, u, w.r, w.S, pl, ctl, 0))) return rc2;
-      if ((rc2 = O::mid(MID_PCG, s, B, w.S, pl, ctl, 0))) return rc2;
-      if ((rc2 = O::inv(INV_PCG, s, B, w.S, w.p, pl, ctl, 0))) return rc2;
+      if ((rc2 = O::fwd(FWD_INIT, s, B, g, beta, f, u, w.S, pl, ctl, 0))) return rc2;
+      if ((rc2 = O::mid(MID_INIT, s, B, w.S, pl, ctl, 0))) return rc2;
+      if ((rc2 = O::inv(INV_INIT, s, B, w.S, w.p, u, pl, ctl, 0))) return rc2;
       // iterations, polled every `chunk` with one chunk of look-ahead
       const int chunk = (n >= 128) ? 2 : 8;
       bool pending = false;
       int ev_i = 0;
       for (int it = 1; it <= opts->max_iter; ++it) {
-        if ((rc2 = O::dot(s, B, g, beta, w.p, ctl, it))) return rc2;
-        if ((rc2 = O::fwd(FWD_ITER, s, B, g, beta, w.p, u, w.r, w.S, pl, ctl, it))) return rc2;
-        if ((rc2 = O::mid(MID_PCG, s, B, w.S, pl, ctl, it))) return rc2;
-        if ((rc2 = O::inv(INV_PCG, s, B, w.S, w.p, pl, ctl, it))) return rc2;
+        // q = A p, p.q, alpha; Q = FFT(q)            (solver.py:162-166)
+        if ((rc2 = O::fwd(FWD_Q, s, B, g, beta, w.p, u, w.S, pl, ctl, it))) return rc2;
+        // R -= alpha Q, stop test, z = P r, r.z, beta (solver.py:168-183)
+        if ((rc2 = O::mid(MID_ITER, s, B, w.S, pl, ctl, it))) return rc2;
+        // u += alpha p, p = z + beta p                (solver.py:167,184)
+        if ((rc2 = O::inv(INV_ITER, s, B, w.S, w.p, u, pl, ctl, it))) return rc2;
         if (it % chunk == 0 || it == opts->max_iter) {
           if (pending) {
             CHK_CUDA(cudaEventSynchronize(ev[ev_i ^ 1]));

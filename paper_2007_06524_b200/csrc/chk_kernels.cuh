@@ -38,6 +38,7 @@ struct RState {
   double mean_f;     // mean removed from f when projected
   double rz[2];      // r.z of the last two iterations (parity-indexed)
   double pq;         // p.Ap of the current iteration
+  double alpha;      // rz_{k-1} / pq_k
   double beta;       // rz_k / rz_{k-1}
   double final_rel;  // last relative residual
   double mean_u;     // final projection (solver.py:169)
@@ -57,12 +58,14 @@ struct Geo {
 
 struct SolveCtl {
   RState* st;        // [B]
+  double2* Rh;       // [B][TILES][N][G*W] residual spectrum, tile-major (PCG)
   double* part;      // [B][maxblk][2]
   double* hist;      // [B][max_iter] or null
   int maxblk;
   int max_iter;
   double tol;
   int prs;           // precond_residual_stopping
+  int dbg;           // timing experiments only (CHK_DEBUG_FLAGS), 0 in production
 };
 
 struct PlanDev {
@@ -466,52 +469,24 @@ __device__ __forceinline__ void c2r_pre(double2* buf, int nrows, int hp,
 }
 
 // ----------------------------------------------------------------------------
-// kernel 1: pq = <p, A p>  (solver.py:162-165)
+// kernel 1: stencil + forward plane transform
 // ----------------------------------------------------------------------------
-template <int N, int G, bool ALLIN>
-__global__ void __launch_bounds__(256, 3) stencil_dot_kernel(Geo g, const double* __restrict__ beta,
-                                                          const double* __restrict__ p,
-                                                          SolveCtl ctl, int it) {
-  constexpr int NR = N / G;
-  __shared__ double scratch[32];
-  const int b = blockIdx.x / (N * G);
-  const int rem = blockIdx.x - b * (N * G);
-  RState* st = ctl.st + b;
-  if (st->status != ST_ACTIVE) return;
-  const int x0 = rem / G, gg = rem - (rem / G) * G;
-  const size_t nb = (size_t)N * N * N;
-  const double* pb = p + b * nb;
-  const double* bb = beta + (size_t)b * g.L * g.L * g.L;
-  double acc = 0.0;
-  constexpr int Q4 = N / 4;
-  for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
-    const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
-    double pc[4], q[4];
-    stencil_quad<ALLIN>(g, pb, bb, x0, gg + G * t, x2, pc, q);
-    acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
-  }
-  double t0, t1;
-  if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G, scratch,
-                   t0, t1)) {
-    if (threadIdx.x == 0) {
-      if (!(t0 > 0.0) || !isfinite(t0)) {  // solver.py:164-165
-        st->status = ST_BREAKDOWN;
-        st->iters = it;
-      }
-      st->pq = t0;
-    }
-  }
-}
+// FWD_APPLY: x rows -> smem.  FWD_INIT: u = 0, f (mean-projected) rows -> smem.
+// FWD_Q: q = A p for the slab's rows (the only stencil of the iteration),
+// <p, q> partials (the last CTA forms alpha = r.z / p.Aq, solver.py:163-166);
+// then R2C along x2 and the x1-group C2C of the smem rows -> spectrum slab S.
+enum : int { FWD_APPLY = 0, FWD_INIT = 1, FWD_Q = 2 };
 
-// ----------------------------------------------------------------------------
-// kernel 2: vector update + forward plane transform
-// ----------------------------------------------------------------------------
-enum : int { FWD_APPLY = 0, FWD_INIT = 1, FWD_ITER = 2 };
+__device__ __forceinline__ void ld4v(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
 
 template <int N, int G, int MODE, bool ALLIN>
 __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __restrict__ beta,
-                                                        const double* __restrict__ src,  // x (APPLY) / f (INIT) / p (ITER)
-                                                        double* __restrict__ u, double* __restrict__ r,
+                                                        const double* __restrict__ src,  // x (APPLY) / f (INIT) / p (Q)
+                                                        double* __restrict__ u,
                                                         double2* __restrict__ S, PlanDev pl,
                                                         SolveCtl ctl, int it) {
   constexpr int NR = N / G;
@@ -526,6 +501,7 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
   const size_t nb = (size_t)N * N * N;
   double* sm = reinterpret_cast<double*>(buf);
   RState* st = (MODE == FWD_APPLY) ? nullptr : ctl.st + b;
+  constexpr int Q4 = N / 4;
 
   if (MODE == FWD_APPLY) {
     for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
@@ -534,81 +510,43 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
     }
   } else if (MODE == FWD_INIT) {
     const int status = st->status;
-    const double shift = st->rhs_projected ? st->mean_f : 0.0;
-    double acc = 0.0;
+    const double shift = st->rhs_projected ? st->mean_f : 0.0;  // solver.py:139-143
     for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
       const int t = i / N, x2 = i - (i / N) * N;
       const size_t idx = b * nb + ((size_t)x0 * N + gg + G * t) * N + x2;
       u[idx] = 0.0;
-      const double rv = __ldg(src + idx) - shift;
-      r[idx] = rv;
-      sm[t * 2 * HP + x2] = rv;
-      acc += rv * rv;
+      sm[t * 2 * HP + x2] = __ldg(src + idx) - shift;
     }
     if (status != ST_ACTIVE) return;
-    double t0, t1;
-    if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G,
-                     scratch, t0, t1)) {
-      if (threadIdx.x == 0) {
-        st->normf = sqrt(t0);
-        if (!(t0 > 0.0)) {  // projected RHS vanished (solver.py:144-148)
-          st->status = ST_CONVERGED;
-          st->iters = 0;
-          st->final_rel = 0.0;
-        }
-      }
-    }
-  } else {  // FWD_ITER
+  } else {  // FWD_Q
     if (st->status != ST_ACTIVE) return;
-    const double alpha = st->rz[(it - 1) & 1] / st->pq;  // solver.py:166
     const double* pb = src + b * nb;
     const double* bb = beta + (size_t)b * g.L * g.L * g.L;
     double acc = 0.0;
-    constexpr int Q4 = N / 4;
     for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
       const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
-      const int x1 = gg + G * t;
-      const size_t idx = b * nb + ((size_t)x0 * N + x1) * N + x2;
       double pc[4], q[4];
-      stencil_quad<ALLIN>(g, pb, bb, x0, x1, x2, pc, q);
-      double2* u2 = reinterpret_cast<double2*>(u + idx);
-      double2* r2 = reinterpret_cast<double2*>(r + idx);
-      double2 ua = u2[0], ub = u2[1], ra = r2[0], rb = r2[1];
-      ua.x += alpha * pc[0]; ua.y += alpha * pc[1];   // solver.py:167
-      ub.x += alpha * pc[2]; ub.y += alpha * pc[3];
-      ra.x -= alpha * q[0]; ra.y -= alpha * q[1];     // solver.py:168
-      rb.x -= alpha * q[2]; rb.y -= alpha * q[3];
-      u2[0] = ua; u2[1] = ub;
-      r2[0] = ra; r2[1] = rb;
+      stencil_quad<ALLIN>(g, pb, bb, x0, gg + G * t, x2, pc, q);
       double2* s2 = reinterpret_cast<double2*>(sm + t * 2 * HP + x2);
-      s2[0] = ra;
-      s2[1] = rb;
-      acc += ((ra.x * ra.x + ra.y * ra.y) + rb.x * rb.x) + rb.y * rb.y;
+      s2[0] = make_double2(q[0], q[1]);
+      s2[1] = make_double2(q[2], q[3]);
+      acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
     }
     double t0, t1;
     if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G,
                      scratch, t0, t1)) {
       if (threadIdx.x == 0) {
-        const double rel = sqrt(t0) / st->normf;  // solver.py:171
-        if (ctl.hist) ctl.hist[(size_t)b * ctl.max_iter + (it - 1)] = rel;
-        st->final_rel = rel;
-        if (!isfinite(rel)) {  // solver.py:172-173
+        if ((!(t0 > 0.0) || !isfinite(t0)) && !ctl.dbg) {  // solver.py:164-165
           st->status = ST_BREAKDOWN;
           st->iters = it;
-        } else if (!ctl.prs && rel <= ctl.tol) {  // solver.py:175-177
-          st->status = ST_CONVERGED;
-          st->iters = it;
-        } else if (!ctl.prs && it >= ctl.max_iter) {
-          st->status = ST_NOT_CONVERGED;
-          st->iters = it;
         }
+        st->pq = t0;
+        st->alpha = st->rz[(it - 1) & 1] / t0;  // solver.py:166
       }
     }
-    // other CTAs of this realization still have to transform their r slab only
-    // if the iteration continues; the decision is known only to the last CTA,
-    // so every CTA transforms (the middle kernel skips converged realizations).
   }
   __syncthreads();
+  if (MODE == FWD_Q && (ctl.dbg & 1)) return;  // debug: skip the transform phase
   // R2C along x2: rows of N reals viewed as N/2 complex (z_m = x_2m + i x_2m+1)
   fft_smem<N2, false, NR>(buf, RowAddr{HP}, pl.tw, N);
   r2c_post<N>(buf, NR, HP, pl.tw);
@@ -627,65 +565,86 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
 }
 
 // ----------------------------------------------------------------------------
-// kernel 3: spectral column pass (x1 group combine + x0), diagonal scaling
+// kernel 2: spectral column pass (x1 group combine + x0), diagonal scaling
 // ----------------------------------------------------------------------------
-enum : int { MID_APPLY = 0, MID_PCG = 1 };
+// MID_APPLY: z = D * X (standalone preconditioner, DC term kept).
+// MID_INIT:  R = X (the spectrum of r0 = f), ||r0||^2 and r0.z0 by Parseval.
+// MID_ITER:  R -= alpha * Q (Q = FFT of q = A p; solver.py:168 in the Fourier
+//            domain -- r is only ever consumed through its spectrum), then
+//            ||r||^2 (stop test, solver.py:171-177), z = D * R with the mean
+//            projection (solver.py:179) and r.z (solver.py:180-183).
+// The residual spectrum R lives in HBM tile-major (one contiguous N x G*W block
+// per column tile), so each CTA streams its own slice.
+enum : int { MID_APPLY = 0, MID_INIT = 1, MID_ITER = 2 };
 
 __host__ __device__ __forceinline__ int mid_dsm_offset(int tile_elems, int gw, int r1) {
   const int a = tile_elems * 16, c = r1 * gw * 8;
   return ((a > c ? a : c) + 15) & ~15;
 }
 
-// A CTA owns W consecutive spectral columns c' of every (x0, group) slab and
-// NB realizations.  The diagonal tile D[pos0][slot] (N x G*W) is evaluated once
-// per CTA -- LKR: D = U0p^T C with C[r][slot] = U1[r][k1] U2[r][k2] (a rank-r1
-// contraction; U0p = U0 with columns in digit-reversed x0 order, so a thread's
-// 4 consecutive pos0 are contiguous) -- and reused for the NB realizations.
-template <int N, int G, int W, int NB, int MODE>
-__global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S, PlanDev pl,
-                                                         SolveCtl ctl, int it, int B) {
-  constexpr int NR = N / G;
-  constexpr int N2 = N / 2;
-  constexpr int H = N2 + 1;
-  constexpr int TILES = NR * H / W;
-  constexpr int GW = G * W;
-  constexpr int RS = GW + 1;
-  extern __shared__ double2 buf[];  // [N][RS] data tile (aliased by the [r1][GW] coefficients)
-  const int doff = mid_dsm_offset(N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
-  double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
-  __shared__ double scratch[32];
-  __shared__ int s_k1[GW], s_k2[GW];
-  __shared__ double2 s_tw[GW];
-  __shared__ int s_any;
-  const int bg = blockIdx.x / TILES;
-  const int tile = blockIdx.x - bg * TILES;
-  const int c0 = tile * W;
-  const int b0 = bg * NB;
-
-  if (MODE == MID_PCG) {
-    if (threadIdx.x == 0) {
-      int any = 0;
-      for (int j = 0; j < NB && b0 + j < B; ++j) any |= (ctl.st[b0 + j].status == ST_ACTIVE);
-      s_any = any;
+// Scalar decisions of one iteration, taken by the last CTA of a realization
+// (rr = ||r||^2, rz = r.z, both already divided by N^3).
+__device__ __forceinline__ void mid_decide(RState* st, const SolveCtl& ctl, int b, int it, double rr,
+                                           double rz) {
+  if (it == 0) {
+    st->normf = sqrt(rr);  // solver.py:132 (after the optional projection, :142)
+    if (!(rr > 0.0)) {     // projected RHS vanished (solver.py:144-148)
+      st->status = ST_CONVERGED;
+      st->iters = 0;
+      st->final_rel = 0.0;
+      return;
     }
-    __syncthreads();
-    if (!s_any) return;
+    st->rz[0] = rz;
+    st->norm_pf = sqrt(fabs(rz));  // solver.py:156
+    st->beta = 0.0;
+    return;
   }
-  // slot s = m*W + w  <->  (k1, k2); group-combine twiddle w_n^(g k') per (g, w)
+  const double rel = sqrt(rr) / st->normf;  // solver.py:171
+  if (ctl.hist) ctl.hist[(size_t)b * ctl.max_iter + (it - 1)] = rel;
+  st->final_rel = rel;
+  if (!isfinite(rel) && !ctl.dbg) {  // solver.py:172-173
+    st->status = ST_BREAKDOWN;
+    st->iters = it;
+    return;
+  }
+  if (!ctl.prs && rel <= ctl.tol) {  // solver.py:175-177
+    st->status = ST_CONVERGED;
+    st->iters = it;
+    return;
+  }
+  st->beta = rz / st->rz[(it - 1) & 1];  // solver.py:184
+  st->rz[it & 1] = rz;
+  if (ctl.prs && sqrt(fabs(rz)) / st->norm_pf <= ctl.tol) {  // solver.py:181-183
+    st->status = ST_CONVERGED;
+    st->iters = it;
+    return;
+  }
+  if (it >= ctl.max_iter) {
+    st->status = ST_NOT_CONVERGED;
+    st->iters = it;
+  }
+}
+
+// Shared prologue of both middle kernels: slot bookkeeping and the diagonal tile.
+template <int N, int G, int W, int MODE>
+__device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, const PlanDev& pl,
+                                             int* s_k1, int* s_k2, double* s_wgt, double2* s_tw) {
+  constexpr int NR = N / G, N2 = N / 2, H = N2 + 1, GW = G * W;
   for (int s = threadIdx.x; s < GW; s += blockDim.x) {
     const int m = dig_freq<G>(s / W), w = s % W;
     const int c = c0 + w;
     const int q1 = c / H, q2 = c - (c / H) * H;
     const int kp = dig_freq<NR>(q1);
     s_k1[s] = kp + m * NR;
-    s_k2[s] = (q2 == N2) ? N2 : dig_freq<N2>(q2);
-    const int gq = s / W;  // as a load slot: group gq, column w
-    s_tw[s] = __ldg(pl.tw + gq * dig_freq<NR>((c0 + w) / H));
+    const int k2 = (q2 == N2) ? N2 : dig_freq<N2>(q2);
+    s_k2[s] = k2;
+    s_wgt[s] = (k2 == 0 || k2 == N2) ? 1.0 : 2.0;
+    s_tw[s] = __ldg(pl.tw + (s / W) * kp);  // as a load slot (group s/W, column w)
   }
   __syncthreads();
-  // ---- diagonal tile ----
   if (pl.kind == KIND_LKR) {
-    double* coef = reinterpret_cast<double*>(buf);  // [r1][GW], aliases the data tile
+    // D = U0p^T C, C[r][slot] = U1[r][k1] U2[r][k2]: rank-r1 contraction, once per CTA
+    double* coef = reinterpret_cast<double*>(buf);
     const double* U1 = pl.U + (size_t)pl.r1 * N;
     const double* U2 = pl.U + (size_t)2 * pl.r1 * N;
     for (int i = threadIdx.x; i < pl.r1 * GW; i += blockDim.x) {
@@ -717,6 +676,7 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
     for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
       const int s = i % GW, pos0 = i / GW;
       const int k0 = dig_freq<N>(pos0);
+      // eigensum order of spectral.py:47-52: (lam_i + lam_j) + lam_k
       const double gsum = (__ldg(pl.lam + k0) + __ldg(pl.lam + s_k1[s])) + __ldg(pl.lam + s_k2[s]);
       double D;
       if (pl.kind == KIND_REGULARIZED && pl.delta > 0.0) {
@@ -728,19 +688,73 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
     }
   }
   __syncthreads();
-  if (MODE == MID_PCG && threadIdx.x < GW) {
-    // mean projection of z (solver.py:153,179): zero-frequency coefficient 0
-    // (pos0 = 0 <-> k0 = 0; slot with k1 = k2 = 0)
+  if (MODE != MID_APPLY && threadIdx.x < GW) {
+    // mean projection of z (solver.py:153,179): the zero-frequency coefficient is 0
     if (s_k1[threadIdx.x] == 0 && s_k2[threadIdx.x] == 0) Dsm[threadIdx.x] = 0.0;
   }
   __syncthreads();
+}
+
+// Residual update + scaling of one spectral element (pos0, slot s).
+template <int MODE>
+__device__ __forceinline__ double2 mid_point(double2 v, double D, double wgt, double scale,
+                                             double alpha, double2* rptr, double& rr, double& rz) {
+  if (MODE == MID_APPLY) return cscale(v, D * scale);
+  double2 R = v;
+  if (MODE == MID_ITER) {
+    const double2 Ro = *rptr;
+    R = make_double2(fma(-alpha, v.x, Ro.x), fma(-alpha, v.y, Ro.y));
+  }
+  *rptr = R;
+  const double m2 = R.x * R.x + R.y * R.y;
+  rr = fma(wgt, m2, rr);
+  rz = fma(wgt * D, m2, rz);
+  return cscale(R, D * scale);
+}
+
+// Shared-memory stage kernel (any n; used for n >= 256).
+template <int N, int G, int W, int NB, int MODE>
+__global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S, PlanDev pl,
+                                                         SolveCtl ctl, int it, int B) {
+  constexpr int NR = N / G;
+  constexpr int N2 = N / 2;
+  constexpr int H = N2 + 1;
+  constexpr int TILES = NR * H / W;
+  constexpr int GW = G * W;
+  constexpr int RS = GW + 1;
+  extern __shared__ double2 buf[];  // [N][RS] data tile (aliased by the [r1][GW] coefficients)
+  const int doff = mid_dsm_offset(N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
+  double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
+  __shared__ double scratch[32];
+  __shared__ int s_k1[GW], s_k2[GW];
+  __shared__ double s_wgt[GW];
+  __shared__ double2 s_tw[GW];
+  __shared__ int s_act[NB];
+  __shared__ double s_alpha[NB];
+  const int bg = blockIdx.x / TILES;
+  const int tile = blockIdx.x - bg * TILES;
+  const int c0 = tile * W;
+  const int b0 = bg * NB;
+  if (threadIdx.x == 0) {
+    int any = 0;
+    for (int j = 0; j < NB; ++j) {
+      const int b = b0 + j;
+      int a = (b < B);
+      if (a && MODE != MID_APPLY) a = (ctl.st[b].status == ST_ACTIVE);
+      s_act[j] = a;
+      s_alpha[j] = (a && MODE == MID_ITER) ? ctl.st[b].alpha : 0.0;
+      any |= a;
+    }
+    scratch[0] = any;
+  }
+  __syncthreads();
+  if (scratch[0] == 0.0) return;
+  mid_prologue<N, G, W, MODE>(buf, Dsm, c0, pl, s_k1, s_k2, s_wgt, s_tw);
 
   const double scale = 2.0 / ((double)N * N * N);
   for (int j = 0; j < NB; ++j) {
+    if (!s_act[j]) continue;
     const int b = b0 + j;
-    if (b >= B) break;
-    RState* st = (MODE == MID_PCG) ? ctl.st + b : nullptr;
-    if (MODE == MID_PCG && st->status != ST_ACTIVE) continue;
     double2* base = S + (size_t)b * N * G * (NR * H);
     for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
       const int w = i % W, gq = (i / W) % G, x0 = i / GW;
@@ -751,17 +765,12 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
     __syncthreads();
     if (G > 1) fft_smem<G, false, N * W>(buf, GAddr<W>{RS}, pl.tw, N);
     fft_smem<N, false, GW>(buf, X0Addr{RS}, pl.tw, N);
-    double acc = 0.0;
+    double rr = 0.0, rz = 0.0;
+    double2* Rt = ctl.Rh + ((size_t)b * TILES + tile) * N * GW;
     for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
       const int s = i % GW, pos0 = i / GW;
-      const double D = Dsm[pos0 * GW + s];
-      const double2 v = buf[pos0 * RS + s];
-      if (MODE == MID_PCG) {
-        const int k2 = s_k2[s];
-        const double wgt = (k2 == 0 || k2 == N2) ? 1.0 : 2.0;
-        acc = fma(wgt * D, v.x * v.x + v.y * v.y, acc);
-      }
-      buf[pos0 * RS + s] = cscale(v, D * scale);
+      buf[pos0 * RS + s] = mid_point<MODE>(buf[pos0 * RS + s], Dsm[pos0 * GW + s], s_wgt[s], scale,
+                                           s_alpha[j], Rt + i, rr, rz);
     }
     __syncthreads();
     fft_smem<N, true, GW>(buf, X0Addr{RS}, pl.tw, N);
@@ -772,38 +781,22 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
       if (G > 1) v = cmulc(v, s_tw[gq * W + w]);
       base[((size_t)x0 * G + gq) * (NR * H) + c0 + w] = v;
     }
-    if (MODE == MID_PCG) {
+    if (MODE != MID_APPLY) {
+      RState* st = ctl.st + b;
       double t0, t1;
-      if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
+      if (reduce2_last(rr, rz, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
                        scratch, t0, t1)) {
-        if (threadIdx.x == 0) {
-          const double rz = t0 / ((double)N * N * N);  // Parseval: r.z = (1/N^3) sum conj(R) D R
-          if (it == 0) {
-            st->rz[0] = rz;
-            st->norm_pf = sqrt(fabs(rz));  // solver.py:156
-            st->beta = 0.0;
-          } else {
-            st->beta = rz / st->rz[(it - 1) & 1];  // solver.py:184
-            st->rz[it & 1] = rz;
-            if (ctl.prs && sqrt(fabs(rz)) / st->norm_pf <= ctl.tol) {  // solver.py:181-183
-              st->status = ST_CONVERGED;
-              st->iters = it;
-            } else if (it >= ctl.max_iter) {
-              st->status = ST_NOT_CONVERGED;
-              st->iters = it;
-            }
-          }
-        }
+        const double inv = 1.0 / ((double)N * N * N);  // Parseval: (1/N^3) sum conj(X) Y
+        if (threadIdx.x == 0) mid_decide(st, ctl, b, it, t0 * inv, t1 * inv);
       }
     } else {
-      __syncthreads();  // buf is reloaded for the next realization
+      __syncthreads();
     }
   }
 }
 
 // ----------------------------------------------------------------------------
-// ----------------------------------------------------------------------------
-// kernel 3b: register-resident spectral column pass (n <= 128)
+// kernel 2b: register-resident spectral column pass (n <= 128)
 // ----------------------------------------------------------------------------
 // In-register in-place DIF / inverse DIT of length L on v[0..L): identical
 // index semantics to fft_smem<L> (digit-reversed output), all loops unrolled.
@@ -847,12 +840,12 @@ __device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restri
 // Phase A (thread = column w, x0 offset j): the G-group combine and the first
 // radix-RA x0 stage straight from/to global memory in registers; phase B
 // (thread = slot s, block of RB = N/RA positions): the remaining x0 stages,
-// the diagonal scaling and the inverse stages in registers.  Shared memory is
-// touched twice per element per direction (one exchange each way).  P
-// realizations are in flight per CTA; NB share one diagonal tile.
+// residual update / diagonal scaling and the inverse stages in registers.
+// Shared memory is touched twice per element per direction (one exchange each
+// way).  P realizations are in flight per CTA; NB share one diagonal tile.
 template <int N, int G, int W, int RA, int NB, int P, int MODE, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* __restrict__ S, PlanDev pl,
-                                                             SolveCtl ctl, int it, int B) {
+                                                                      SolveCtl ctl, int it, int B) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
@@ -873,6 +866,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
   __shared__ double s_wgt[GW];
   __shared__ double2 s_tw[GW];
   __shared__ int s_act[NB];
+  __shared__ double s_alpha[NB];
   const int bg = blockIdx.x / TILES;
   const int tile = blockIdx.x - bg * TILES;
   const int c0 = tile * W;
@@ -883,79 +877,29 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
     for (int j = 0; j < NB; ++j) {
       const int b = b0 + j;
       int a = (b < B);
-      if (a && MODE == MID_PCG) a = (ctl.st[b].status == ST_ACTIVE);
+      if (a && MODE != MID_APPLY) a = (ctl.st[b].status == ST_ACTIVE);
       s_act[j] = a;
+      s_alpha[j] = (a && MODE == MID_ITER) ? ctl.st[b].alpha : 0.0;
       any |= a;
     }
     scratch[0] = any;
   }
   __syncthreads();
   if (scratch[0] == 0.0) return;
-  for (int s = threadIdx.x; s < GW; s += blockDim.x) {
-    const int m = dig_freq<G>(s / W), w = s % W;
-    const int c = c0 + w;
-    const int q1 = c / H, q2 = c - (c / H) * H;
-    const int kp = dig_freq<NR>(q1);
-    s_k1[s] = kp + m * NR;
-    const int k2 = (q2 == N2) ? N2 : dig_freq<N2>(q2);
-    s_k2[s] = k2;
-    s_wgt[s] = (k2 == 0 || k2 == N2) ? 1.0 : 2.0;
-    s_tw[s] = __ldg(pl.tw + (s / W) * kp);  // as a load slot (group s/W, column w)
-  }
-  __syncthreads();
-  // ---- diagonal tile (once per CTA) ----
-  if (pl.kind == KIND_LKR) {
-    double* coef = reinterpret_cast<double*>(buf);
-    const double* U1 = pl.U + (size_t)pl.r1 * N;
-    const double* U2 = pl.U + (size_t)2 * pl.r1 * N;
-    for (int i = threadIdx.x; i < pl.r1 * GW; i += blockDim.x) {
-      const int s = i % GW, rr = i / GW;
-      coef[rr * GW + s] = __ldg(U1 + rr * N + s_k1[s]) * __ldg(U2 + rr * N + s_k2[s]);
-    }
-    __syncthreads();
-    constexpr int PQ = N / 4, SQ = GW / 2;
-    for (int i = threadIdx.x; i < PQ * SQ; i += blockDim.x) {
-      const int sq = i % SQ, pq = i / SQ;
-      double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-      const double* up = pl.Up + 4 * pq;
-      for (int rr = 0; rr < pl.r1; ++rr) {
-        const double2 ua = __ldg(reinterpret_cast<const double2*>(up + (size_t)rr * N));
-        const double2 ub = __ldg(reinterpret_cast<const double2*>(up + (size_t)rr * N) + 1);
-        const double2 cc = *reinterpret_cast<const double2*>(coef + rr * GW + 2 * sq);
-        acc[0][0] = fma(ua.x, cc.x, acc[0][0]); acc[0][1] = fma(ua.x, cc.y, acc[0][1]);
-        acc[1][0] = fma(ua.y, cc.x, acc[1][0]); acc[1][1] = fma(ua.y, cc.y, acc[1][1]);
-        acc[2][0] = fma(ub.x, cc.x, acc[2][0]); acc[2][1] = fma(ub.x, cc.y, acc[2][1]);
-        acc[3][0] = fma(ub.y, cc.x, acc[3][0]); acc[3][1] = fma(ub.y, cc.y, acc[3][1]);
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        Dsm[(4 * pq + a) * GW + 2 * sq] = acc[a][0];
-        Dsm[(4 * pq + a) * GW + 2 * sq + 1] = acc[a][1];
-      }
-    }
-  } else {
-    for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
-      const int s = i % GW, pos0 = i / GW;
-      const int k0 = dig_freq<N>(pos0);
-      const double gsum = (__ldg(pl.lam + k0) + __ldg(pl.lam + s_k1[s])) + __ldg(pl.lam + s_k2[s]);
-      double D;
-      if (pl.kind == KIND_REGULARIZED && pl.delta > 0.0) {
-        D = 1.0 / (gsum + pl.delta);
-      } else {
-        D = (gsum > 0.0) ? 1.0 / gsum : 0.0;
-      }
-      Dsm[pos0 * GW + s] = D;
-    }
-  }
-  __syncthreads();
-  if (MODE == MID_PCG && threadIdx.x < GW) {
-    if (s_k1[threadIdx.x] == 0 && s_k2[threadIdx.x] == 0) Dsm[threadIdx.x] = 0.0;  // mean projection
-  }
-  __syncthreads();
+  mid_prologue<N, G, W, MODE>(buf, Dsm, c0, pl, s_k1, s_k2, s_wgt, s_tw);
 
   const double scale = 2.0 / ((double)N * N * N);
   const int ntab = N;
   for (int c = 0; c < NB / P; ++c) {
+    // warm L2 with the next chunk's tile rows (W * 16 B per (x0, group) row)
+    if (c + 1 < NB / P) {
+      for (int i = threadIdx.x; i < P * N * G; i += blockDim.x) {
+        const int pr = i / (N * G), rr = i - pr * (N * G);
+        if (s_act[(c + 1) * P + pr])
+          bulk_prefetch_l2(S + (size_t)(b0 + (c + 1) * P + pr) * N * G * (NR * H) + (size_t)rr * (NR * H) + c0,
+                           W * sizeof(double2));
+      }
+    }
     // ---- phase A forward: global -> registers -> smem ----
     for (int item = threadIdx.x; item < P * ITEMS_A; item += blockDim.x) {
       const int pr = item / ITEMS_A, ia = item - pr * ITEMS_A;
@@ -997,10 +941,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
       }
     }
     __syncthreads();
-    // ---- phase B: remaining stages, diagonal, inverse (registers) ----
-    double acc[P];
+    // ---- phase B: remaining stages, residual update / diagonal, inverse ----
+    double accr[P], accz[P];
 #pragma unroll
-    for (int pr = 0; pr < P; ++pr) acc[pr] = 0.0;
+    for (int pr = 0; pr < P; ++pr) accr[pr] = accz[pr] = 0.0;
     for (int item = threadIdx.x; item < P * ITEMS_B; item += blockDim.x) {
       const int pr = item / ITEMS_B, ib = item - pr * ITEMS_B;
       if (!s_act[c * P + pr]) continue;
@@ -1010,17 +954,19 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
 #pragma unroll
       for (int e = 0; e < RB; ++e) v[e] = row[e * RS];
       reg_fft<RB, false>(v, pl.tw, ntab);
-      double a = 0.0;
+      double rr = 0.0, rz = 0.0;
       const double wgt = s_wgt[s];
+      const double al = s_alpha[c * P + pr];
+      double2* Rt = ctl.Rh + ((size_t)(b0 + c * P + pr) * TILES + tile) * N * GW + (blk * RB) * GW + s;
 #pragma unroll
-      for (int e = 0; e < RB; ++e) {
-        const double D = Dsm[(blk * RB + e) * GW + s];
-        if (MODE == MID_PCG) a = fma(wgt * D, v[e].x * v[e].x + v[e].y * v[e].y, a);
-        v[e] = cscale(v[e], D * scale);
-      }
+      for (int e = 0; e < RB; ++e)
+        v[e] = mid_point<MODE>(v[e], Dsm[(blk * RB + e) * GW + s], wgt, scale, al, Rt + e * GW, rr, rz);
 #pragma unroll
       for (int pr2 = 0; pr2 < P; ++pr2)
-        if (pr2 == pr) acc[pr2] += a;
+        if (pr2 == pr) {
+          accr[pr2] += rr;
+          accz[pr2] += rz;
+        }
       reg_fft<RB, true>(v, pl.tw, ntab);
 #pragma unroll
       for (int e = 0; e < RB; ++e) row[e * RS] = v[e];
@@ -1066,34 +1012,18 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
 #pragma unroll
         for (int g = 0; g < G; ++g) base[((size_t)(j + JA * t) * G + g) * (NR * H)] = v[g][t];
     }
-    // ---- per-realization Parseval reductions ----
-    if (MODE == MID_PCG) {
+    // ---- per-realization Parseval reductions and decisions ----
+    if (MODE != MID_APPLY) {
 #pragma unroll
       for (int pr = 0; pr < P; ++pr) {
         const int b = b0 + c * P + pr;
         if (!s_act[c * P + pr]) continue;
         RState* st = ctl.st + b;
         double t0, t1;
-        if (reduce2_last(acc[pr], 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
-                         scratch, t0, t1)) {
-          if (threadIdx.x == 0) {
-            const double rz = t0 / ((double)N * N * N);
-            if (it == 0) {
-              st->rz[0] = rz;
-              st->norm_pf = sqrt(fabs(rz));
-              st->beta = 0.0;
-            } else {
-              st->beta = rz / st->rz[(it - 1) & 1];
-              st->rz[it & 1] = rz;
-              if (ctl.prs && sqrt(fabs(rz)) / st->norm_pf <= ctl.tol) {
-                st->status = ST_CONVERGED;
-                st->iters = it;
-              } else if (it >= ctl.max_iter) {
-                st->status = ST_NOT_CONVERGED;
-                st->iters = it;
-              }
-            }
-          }
+        if (reduce2_last(accr[pr], accz[pr], ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile,
+                         TILES, scratch, t0, t1)) {
+          const double inv = 1.0 / ((double)N * N * N);
+          if (threadIdx.x == 0) mid_decide(st, ctl, b, it, t0 * inv, t1 * inv);
         }
       }
     }
@@ -1101,55 +1031,103 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
   }
 }
 
-// kernel 4: inverse plane transform + direction update
 // ----------------------------------------------------------------------------
-enum : int { INV_APPLY = 0, INV_PCG = 1 };
+// kernel 3: inverse plane transform + solution / direction update
+// ----------------------------------------------------------------------------
+// INV_APPLY: out = z.  INV_INIT: p = z (solver.py:154).
+// INV_ITER:  u += alpha_k p_k (solver.py:167; deferred here, where p_k is read
+//            anyway) and, while the solve continues, p = z + beta p_k
+//            (solver.py:184).  At the stopping iteration only u is updated.
+enum : int { INV_APPLY = 0, INV_INIT = 1, INV_ITER = 2 };
+
+__device__ __forceinline__ void ldv4(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p)
+               : "memory");
+}
+__device__ __forceinline__ void stv4(double* p, const double (&v)[4]) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
 
 template <int N, int G, int MODE>
 __global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restrict__ S,
-                                                        double* __restrict__ out, PlanDev pl,
-                                                        SolveCtl ctl, int it) {
+                                                        double* __restrict__ out, double* __restrict__ u,
+                                                        PlanDev pl, SolveCtl ctl, int it) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
   constexpr int HP = H;
   extern __shared__ double2 buf[];
+  __shared__ alignas(8) uint64_t bar;
   const int b = blockIdx.x / (N * G);
   const int rem = blockIdx.x - b * (N * G);
   const int x0 = rem / G, gg = rem - (rem / G) * G;
   const size_t nb = (size_t)N * N * N;
-  double beta = 0.0;
-  if (MODE == INV_PCG) {
-    RState* st = ctl.st + b;
-    if (st->status != ST_ACTIVE) return;
-    beta = st->beta;
+  double alpha = 0.0, beta = 0.0;
+  bool do_p = true, do_u = false;
+  if (MODE != INV_APPLY) {
+    const RState* st = ctl.st + b;
+    const int status = st->status;
+    do_p = (status == ST_ACTIVE);
+    if (MODE == INV_ITER) {
+      do_u = do_p || ((status == ST_CONVERGED || status == ST_NOT_CONVERGED) && st->iters == it);
+      alpha = st->alpha;
+      beta = st->beta;
+    }
+    if (!do_p && !do_u) return;
   }
-  const double2* srcp = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
-  __shared__ alignas(8) uint64_t bar;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_arrive_expect_tx(&bar, (uint32_t)(NR * H * sizeof(double2)));
-    bulk_g2s(buf, srcp, (uint32_t)(NR * H * sizeof(double2)), &bar);
+  if (do_p) {
+    const double2* srcp = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_arrive_expect_tx(&bar, (uint32_t)(NR * H * sizeof(double2)));
+      bulk_g2s(buf, srcp, (uint32_t)(NR * H * sizeof(double2)), &bar);
+    }
   }
-  if (MODE == INV_PCG && it > 0 && threadIdx.x < NR) {
-    // p rows of this slab are read after the transforms: warm L2 now
-    bulk_prefetch_l2(out + b * nb + ((size_t)x0 * N + gg + G * threadIdx.x) * N, N * sizeof(double));
+  if (MODE == INV_ITER && threadIdx.x < NR) {
+    // p and u rows of this slab are read after the transforms: warm L2 now
+    const size_t ro = b * nb + ((size_t)x0 * N + gg + G * threadIdx.x) * N;
+    bulk_prefetch_l2(out + ro, N * sizeof(double));
+    bulk_prefetch_l2(u + ro, N * sizeof(double));
   }
-  __syncthreads();  // barrier initialised before anyone waits
-  mbar_wait(&bar, 0);
-  fft_smem<NR, true, H>(buf, ColAddr{HP}, pl.tw, N);
-  c2r_pre<N>(buf, NR, HP, pl.tw);
-  __syncthreads();
-  fft_smem<N2, true, NR>(buf, RowAddr{HP}, pl.tw, N);
+  if (do_p) {
+    __syncthreads();  // barrier initialised before anyone waits
+    mbar_wait(&bar, 0);
+    fft_smem<NR, true, H>(buf, ColAddr{HP}, pl.tw, N);
+    c2r_pre<N>(buf, NR, HP, pl.tw);
+    __syncthreads();
+    fft_smem<N2, true, NR>(buf, RowAddr{HP}, pl.tw, N);
+  }
   const double* sm = reinterpret_cast<const double*>(buf);
-  for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
-    const int t = i / N, x2 = i - (i / N) * N;
+  constexpr int Q4 = N / 4;
+  for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
+    const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
     const size_t idx = b * nb + ((size_t)x0 * N + gg + G * t) * N + x2;
-    const double z = sm[t * 2 * HP + x2];
-    if (MODE == INV_APPLY) {
-      out[idx] = z;
+    double z[4] = {0.0, 0.0, 0.0, 0.0};
+    if (do_p) {
+      const double2 za = *reinterpret_cast<const double2*>(sm + t * 2 * HP + x2);
+      const double2 zb = *reinterpret_cast<const double2*>(sm + t * 2 * HP + x2 + 2);
+      z[0] = za.x; z[1] = za.y; z[2] = zb.x; z[3] = zb.y;
+    }
+    if (MODE == INV_APPLY || MODE == INV_INIT) {
+      stv4(out + idx, z);
     } else {
-      out[idx] = (it == 0) ? z : z + beta * out[idx];  // solver.py:154,184
+      double po[4], uo[4];
+      ldv4(out + idx, po);
+      if (do_u) {
+        ldv4(u + idx, uo);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) uo[e] = fma(alpha, po[e], uo[e]);  // u += step p
+        stv4(u + idx, uo);
+      }
+      if (do_p) {
+        double pn[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pn[e] = fma(beta, po[e], z[e]);  // p = z + beta p
+        stv4(out + idx, pn);
+      }
     }
   }
 }
