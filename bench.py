@@ -275,8 +275,15 @@ def run_ours(args):
         traffic = None
         prof_json = os.path.join(REPO, "profiles", "ncu_traffic.json")
         if dom and os.path.exists(prof_json):
-            tj = json.load(open(prof_json)).get(f"config{cfg_id}", {})
-            traffic = tj.get(dom)
+            # ncu --set full dram__bytes_read+write of the same kernel (profiles/), per DOF,
+            # scaled to the DOF one launch processes on average in this run
+            ncu_name = {"fwd_plane": "fwd_plane_kernel", "mid_column": "mid_column_reg_kernel",
+                        "inv_plane": "inv_plane_kernel"}.get(dom)
+            tj = json.load(open(prof_json)).get(f"config{cfg_id}", {}).get(ncu_name)
+            if tj:
+                per_launch_dof = dof_it_rank / max(1, per_kernel[dom]["launches"])
+                traffic = {"bytes_per_launch": round(tj["dram_bytes_per_dof"] * per_launch_dof),
+                           "bytes_per_dof": tj["dram_bytes_per_dof"], "source": tj["source"]}
         roofline = None
         if dom:
             d = per_kernel[dom]
