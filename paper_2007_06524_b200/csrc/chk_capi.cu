@@ -104,8 +104,8 @@ struct Cfg;
 template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8,  NB = 4, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 1; };
-template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 8, REG = 1, RA = 8, P = 1; };
-template <> struct Cfg<128> { static constexpr int G = 2,  W = 8,  NB = 8, REG = 1, RA = 8, P = 1; };
+template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 16, REG = 1, RA = 8, P = 1; };
+template <> struct Cfg<128> { static constexpr int G = 2,  W = 8,  NB = 16, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 4, REG = 0, RA = 1, P = 1; };
 template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2, REG = 0, RA = 1, P = 1; };
 

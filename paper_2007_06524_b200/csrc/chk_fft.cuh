@@ -175,4 +175,32 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
   return r;
 }
 
+// Two block sums in one pass (results valid in every thread). scratch >= 64 doubles.
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* scratch) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) {
+    scratch[wid] = a;
+    scratch[32 + wid] = b;
+  }
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double ta = (threadIdx.x < nw) ? scratch[threadIdx.x] : 0.0;
+  double tb = (threadIdx.x < nw) ? scratch[32 + threadIdx.x] : 0.0;
+  if (wid == 0) {
+    ta = warp_sum(ta);
+    tb = warp_sum(tb);
+  }
+  if (threadIdx.x == 0) {
+    scratch[0] = ta;
+    scratch[32] = tb;
+  }
+  __syncthreads();
+  a = scratch[0];
+  b = scratch[32];
+  __syncthreads();
+}
+
 }  // namespace chk

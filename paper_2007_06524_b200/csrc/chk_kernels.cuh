@@ -255,25 +255,40 @@ __device__ __forceinline__ void stencil4(const Geo& g, const RowCtx& rc, int x2s
 // alpha = 1/2, the BASELINE configurations): F = beta(cell) everywhere, the
 // quad x2s..x2s+3 shares one cell column, and nodes 1..3 of the quad share
 // their six edge weights.  Same formulas and summation order as stencil4.
+// Rows are read with 256-bit loads; when one warp (segment) covers whole rows
+// (n = 64, 128) the x2 halo comes from the neighbouring lane by shuffle.
+__device__ __forceinline__ void ldg4v(const double* p, double (&v)[4]) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+
+template <int N>
 __device__ __forceinline__ void stencil4_allin(const Geo& g, const double* __restrict__ p,
                                                const double* __restrict__ beta, int x0, int x1,
                                                int x2s, double (&pc)[4], double (&q)[4]) {
-  const int n = g.n, nm = n - 1;
-  const long long nn = (long long)n * n;
-  const long long row = (long long)x0 * nn + (long long)x1 * n;
+  constexpr int nm = N - 1;
+  constexpr int Q4 = N / 4;
+  constexpr bool SHFL = (Q4 == 16 || Q4 == 32);
+  constexpr long long nn = (long long)N * N;
+  const long long row = (long long)x0 * nn + (long long)x1 * N;
   const long long d0m = (x0 == 0) ? (long long)nm * nn : -nn;
   const long long d0p = (x0 == nm) ? -(long long)nm * nn : nn;
-  const long long d1m = (x1 == 0) ? (long long)nm * n : -(long long)n;
-  const long long d1p = (x1 == nm) ? -(long long)nm * n : (long long)n;
+  const long long d1m = (x1 == 0) ? (long long)nm * N : -(long long)N;
+  const long long d1p = (x1 == nm) ? -(long long)nm * N : (long long)N;
   const double* pr = p + row + x2s;
   double xm[4], xp[4], ym[4], yp[4];
-  ld4(pr, pc);
-  ld4(pr + d0m, xm);
-  ld4(pr + d0p, xp);
-  ld4(pr + d1m, ym);
-  ld4(pr + d1p, yp);
-  const double pl = __ldg(p + row + ((x2s - 1) & nm));
-  const double prr = __ldg(p + row + ((x2s + 4) & nm));
+  ldg4v(pr, pc);
+  ldg4v(pr + d0m, xm);
+  ldg4v(pr + d0p, xp);
+  ldg4v(pr + d1m, ym);
+  ldg4v(pr + d1p, yp);
+  double pl, prr;
+  if constexpr (SHFL) {
+    pl = __shfl_sync(0xffffffffu, pc[3], (threadIdx.x - 1) & (Q4 - 1), Q4);
+    prr = __shfl_sync(0xffffffffu, pc[0], (threadIdx.x + 1) & (Q4 - 1), Q4);
+  } else {
+    pl = __ldg(p + row + ((x2s - 1) & nm));
+    prr = __ldg(p + row + ((x2s + 4) & nm));
+  }
   // cell rows (c(j0), c(j1), :) for j0 in {x0-1, x0}, j1 in {x1-1, x1}
   const int L = g.L, sh = g.sh;
   const int c0m = ((x0 - 1) & nm) >> sh, c00 = x0 >> sh;
@@ -309,12 +324,12 @@ __device__ __forceinline__ void stencil4_allin(const Geo& g, const double* __res
   }
 }
 
-template <bool ALLIN>
+template <int N, bool ALLIN>
 __device__ __forceinline__ void stencil_quad(const Geo& g, const double* __restrict__ p,
                                              const double* __restrict__ beta, int x0, int x1,
                                              int x2s, double (&pc)[4], double (&q)[4]) {
   if constexpr (ALLIN) {
-    stencil4_allin(g, p, beta, x0, x1, x2s, pc, q);
+    stencil4_allin<N>(g, p, beta, x0, x1, x2s, pc, q);
   } else {
     const RowCtx rc = make_row(p, beta, g, x0, x1);
     stencil4(g, rc, x2s, pc, q);
@@ -341,7 +356,7 @@ __global__ void __launch_bounds__(256) stencil_apply_kernel(Geo g, const double*
     const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
     const int x1 = gg + G * t;
     double pc[4], q[4];
-    stencil_quad<ALLIN>(g, xb, bb, x0, x1, x2, pc, q);
+    stencil_quad<N, ALLIN>(g, xb, bb, x0, x1, x2, pc, q);
     double2* yo = reinterpret_cast<double2*>(y + b * nb + ((size_t)x0 * N + x1) * N + x2);
     yo[0] = make_double2(q[0], q[1]);
     yo[1] = make_double2(q[2], q[3]);
@@ -526,7 +541,7 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
     for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
       const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
       double pc[4], q[4];
-      stencil_quad<ALLIN>(g, pb, bb, x0, gg + G * t, x2, pc, q);
+      stencil_quad<N, ALLIN>(g, pb, bb, x0, gg + G * t, x2, pc, q);
       double2* s2 = reinterpret_cast<double2*>(sm + t * 2 * HP + x2);
       s2[0] = make_double2(q[0], q[1]);
       s2[1] = make_double2(q[2], q[3]);
