@@ -136,6 +136,53 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
                               int32_t* status, int32_t* rhs_projected, double* history,
                               void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Slab decomposition of one grid over `nranks` GPUs (the
+ * realization loop of ensemble_run, homogenize.py:133-182, shards instead).
+ * Rank r owns planes x0 in [r n/P, (r+1) n/P) of p, u, f and one chunk of the
+ * spectral columns.  The caller drives the iteration phase by phase and runs
+ * the collectives in between (torch.distributed / NCCL):
+ *   STATS, allreduce(red), STATS_DECIDE, FWD_INIT, all_to_all(xa -> xb),
+ *   MID(0), allreduce(red), MID_DECIDE(0), all_to_all(xb -> xa), INV(0),
+ *   then per iteration k: halo exchange of p (first/last local planes),
+ *   FWD_Q(k), allreduce(red), ALPHA_DECIDE(k), all_to_all(xa -> xb), MID(k),
+ *   allreduce(red), MID_DECIDE(k), all_to_all(xb -> xa), INV(k); finally
+ *   MEANU, allreduce(red), MEANU_APPLY.
+ * xa / xb: device exchange buffers of chk_slab_exchange_elems complex128
+ * laid out [chunk s][b][local plane][x1 group][ncols]; all_to_all with equal
+ * splits maps x0 slabs <-> column chunks.  red: device [B][4] doubles; phases
+ * that produce rank-local sums zero it first; allreduce(SUM) it over ranks.
+ * halo_lo / halo_hi: device [B][n*n] planes x0 = r n/P - 1 and (r+1) n/P.
+ * ------------------------------------------------------------------------- */
+typedef struct chk_slab {
+  int32_t nranks; /* P: must divide n and the middle-pass tile count */
+  int32_t rank;
+} chk_slab;
+
+#define CHK_SLAB_STATS 0
+#define CHK_SLAB_STATS_DECIDE 1
+#define CHK_SLAB_FWD_INIT 2
+#define CHK_SLAB_MID 3
+#define CHK_SLAB_MID_DECIDE 4
+#define CHK_SLAB_INV 5
+#define CHK_SLAB_FWD_Q 6
+#define CHK_SLAB_ALPHA_DECIDE 7
+#define CHK_SLAB_MEANU 8
+#define CHK_SLAB_MEANU_APPLY 9
+
+size_t chk_slab_exchange_elems(const chk_grid* grid, const chk_slab* slab, int32_t B);
+size_t chk_slab_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, const chk_slab* slab,
+                                int32_t B, int32_t max_iter);
+int32_t chk_slab_phase(const chk_grid* grid, const chk_precond_plan* plan, const chk_slab* slab,
+                       int32_t phase, int32_t it, const double* beta, const double* f, double* u, double* p,
+                       void* xa, void* xb, const double* halo_lo, const double* halo_hi, double* red,
+                       int32_t B, const chk_pcg_opts* opts, void* workspace, size_t workspace_bytes,
+                       void* stream);
+/* Per-realization status words (device -> host, synchronous on `stream`). */
+int32_t chk_slab_read_state(const chk_grid* grid, const chk_slab* slab, int32_t B, int32_t max_iter,
+                            void* workspace, int32_t* iterations, double* final_rel, int32_t* status,
+                            int32_t* rhs_projected, double* history, void* stream);
+
 /* Number of kernels launched by the last chk_pcg_solve_batched on this thread
  * (the bench's gpu_launches evidence). */
 int64_t chk_last_launch_count(void);

@@ -123,6 +123,13 @@ struct Ops {
     return (size_t)mid_dsm_offset(N * (G * W + 1), G * W, r1) + (size_t)N * G * W * sizeof(double);
   }
   static int maxblk() { return PLANE_BLOCKS > TILES ? PLANE_BLOCKS : TILES; }
+  // single-GPU layout: all planes, one column chunk, periodic halo inside p
+  static SlabGeo whole() { return SlabGeo{N, 0, 1, NR * H, 0, TILES, nullptr, nullptr}; }
+  // rank `rank` of `P` owning n/P consecutive planes and column chunk `rank`
+  static SlabGeo slab(int P, int rank, const double* lo, const double* hi) {
+    return SlabGeo{N / P, rank * (N / P), P, NR * H / P, rank * (TILES / P), TILES / P, lo, hi};
+  }
+  static bool slab_ok(int P) { return P >= 1 && N % P == 0 && (N / P) >= 1 && TILES % P == 0 && P <= 64; }
 
   template <class K>
   static cudaError_t allow_smem(K kernel, size_t bytes) {
@@ -132,72 +139,73 @@ struct Ops {
   }
 
   static int fwd(int mode, cudaStream_t s, int B, Geo g, const double* beta, const double* src,
-                 double* u, double2* S, PlanDev pl, SolveCtl ctl, int it) {
+                 double* u, double2* S, PlanDev pl, SolveCtl ctl, int it, SlabGeo sg = whole()) {
     const size_t sm = plane_smem();
-    dim3 grid(B * PLANE_BLOCKS), block(256);
+    dim3 grid(B * sg.nloc * G), block(256);
     ProfScope ps(1, s);
     if (mode == FWD_APPLY) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_APPLY, false>, sm));
-      fwd_plane_kernel<N, G, FWD_APPLY, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, it);
+      fwd_plane_kernel<N, G, FWD_APPLY, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, sg, B, it);
     } else if (mode == FWD_INIT) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_INIT, false>, sm));
-      fwd_plane_kernel<N, G, FWD_INIT, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, it);
+      fwd_plane_kernel<N, G, FWD_INIT, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, sg, B, it);
     } else if (allin(g)) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_Q, true>, sm));
-      fwd_plane_kernel<N, G, FWD_Q, true><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, it);
+      fwd_plane_kernel<N, G, FWD_Q, true><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, sg, B, it);
     } else {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_Q, false>, sm));
-      fwd_plane_kernel<N, G, FWD_Q, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, it);
+      fwd_plane_kernel<N, G, FWD_Q, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, sg, B, it);
     }
     CHK_LAUNCHED();
     return CHK_OK;
   }
   template <int NBX, int MODE>
-  static int mid_launch(cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it) {
+  static int mid_launch(cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it, SlabGeo sg) {
     const int r1 = pl.kind == KIND_LKR ? pl.r1 : 0;
-    dim3 grid(((B + NBX - 1) / NBX) * TILES), block(256);
+    dim3 grid(((B + NBX - 1) / NBX) * sg.tiles), block(256);
     if constexpr (REG) {
       constexpr int PX = (NBX == 1) ? 1 : P;
       constexpr int NT = 128 * PX;
       const size_t sm = (size_t)mid_dsm_offset(PX * N * (G * W + 1), G * W, r1) + (size_t)N * G * W * sizeof(double);
       CHK_CUDA(allow_smem(mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT>, sm));
-      mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT><<<grid, NT, sm, s>>>(S, pl, ctl, it, B);
+      mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT><<<grid, NT, sm, s>>>(S, pl, ctl, sg, it, B);
     } else {
       const size_t sm = mid_smem(r1);
       CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, NBX, MODE>, sm));
-      mid_column_kernel<N, G, W, NBX, MODE><<<grid, block, sm, s>>>(S, pl, ctl, it, B);
+      mid_column_kernel<N, G, W, NBX, MODE><<<grid, block, sm, s>>>(S, pl, ctl, sg, it, B);
     }
     return CHK_OK;
   }
-  static int mid(int mode, cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it) {
+  static int mid(int mode, cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it,
+                 SlabGeo sg = whole()) {
     ProfScope ps(2, s);
     // amortise the diagonal over NB realizations when that still fills the GPU
-    const bool wide = ((B + NB - 1) / NB) * TILES >= 2 * 148;
+    const bool wide = ((B + NB - 1) / NB) * sg.tiles >= 2 * 148;
     int rc;
     if (mode == MID_APPLY)
-      rc = wide ? mid_launch<NB, MID_APPLY>(s, B, S, pl, ctl, it) : mid_launch<1, MID_APPLY>(s, B, S, pl, ctl, it);
+      rc = wide ? mid_launch<NB, MID_APPLY>(s, B, S, pl, ctl, it, sg) : mid_launch<1, MID_APPLY>(s, B, S, pl, ctl, it, sg);
     else if (mode == MID_INIT)
-      rc = wide ? mid_launch<NB, MID_INIT>(s, B, S, pl, ctl, it) : mid_launch<1, MID_INIT>(s, B, S, pl, ctl, it);
+      rc = wide ? mid_launch<NB, MID_INIT>(s, B, S, pl, ctl, it, sg) : mid_launch<1, MID_INIT>(s, B, S, pl, ctl, it, sg);
     else
-      rc = wide ? mid_launch<NB, MID_ITER>(s, B, S, pl, ctl, it) : mid_launch<1, MID_ITER>(s, B, S, pl, ctl, it);
+      rc = wide ? mid_launch<NB, MID_ITER>(s, B, S, pl, ctl, it, sg) : mid_launch<1, MID_ITER>(s, B, S, pl, ctl, it, sg);
     if (rc) return rc;
     CHK_LAUNCHED();
     return CHK_OK;
   }
   static int inv(int mode, cudaStream_t s, int B, const double2* S, double* out, double* u,
-                 PlanDev pl, SolveCtl ctl, int it) {
+                 PlanDev pl, SolveCtl ctl, int it, SlabGeo sg = whole()) {
     const size_t sm = plane_smem();
-    dim3 grid(B * PLANE_BLOCKS), block(256);
+    dim3 grid(B * sg.nloc * G), block(256);
     ProfScope ps(3, s);
     if (mode == INV_APPLY) {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_APPLY>, sm));
-      inv_plane_kernel<N, G, INV_APPLY><<<grid, block, sm, s>>>(S, out, u, pl, ctl, it);
+      inv_plane_kernel<N, G, INV_APPLY><<<grid, block, sm, s>>>(S, out, u, pl, ctl, sg, B, it);
     } else if (mode == INV_INIT) {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_INIT>, sm));
-      inv_plane_kernel<N, G, INV_INIT><<<grid, block, sm, s>>>(S, out, u, pl, ctl, it);
+      inv_plane_kernel<N, G, INV_INIT><<<grid, block, sm, s>>>(S, out, u, pl, ctl, sg, B, it);
     } else {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_ITER>, sm));
-      inv_plane_kernel<N, G, INV_ITER><<<grid, block, sm, s>>>(S, out, u, pl, ctl, it);
+      inv_plane_kernel<N, G, INV_ITER><<<grid, block, sm, s>>>(S, out, u, pl, ctl, sg, B, it);
     }
     CHK_LAUNCHED();
     return CHK_OK;
@@ -211,13 +219,13 @@ struct Ops {
     CHK_LAUNCHED();
     return CHK_OK;
   }
-  static int rhs_stats(cudaStream_t s, int B, const double* f, SolveCtl ctl) {
-    rhs_stats_kernel<N, G><<<B * PLANE_BLOCKS, 256, 0, s>>>(f, ctl);
+  static int rhs_stats(cudaStream_t s, int B, const double* f, SolveCtl ctl, SlabGeo sg = whole()) {
+    rhs_stats_kernel<N, G><<<B * sg.nloc * G, 256, 0, s>>>(f, ctl, sg);
     CHK_LAUNCHED();
     return CHK_OK;
   }
-  static int mean_u(cudaStream_t s, int B, const double* u, SolveCtl ctl) {
-    mean_u_kernel<N, G><<<B * PLANE_BLOCKS, 256, 0, s>>>(u, ctl);
+  static int mean_u(cudaStream_t s, int B, const double* u, SolveCtl ctl, SlabGeo sg = whole()) {
+    mean_u_kernel<N, G><<<B * sg.nloc * G, 256, 0, s>>>(u, ctl, sg);
     CHK_LAUNCHED();
     return CHK_OK;
   }
@@ -229,15 +237,15 @@ struct Ops {
   }
 };
 
-#define CHK_DISPATCH(n, EXPR)                       \
-  switch (n) {                                      \
-    case 8:   { using O = Ops<8>;   EXPR; } break;  \
-    case 16:  { using O = Ops<16>;  EXPR; } break;  \
-    case 32:  { using O = Ops<32>;  EXPR; } break;  \
-    case 64:  { using O = Ops<64>;  EXPR; } break;  \
-    case 128: { using O = Ops<128>; EXPR; } break;  \
-    case 256: { using O = Ops<256>; EXPR; } break;  \
-    case 512: { using O = Ops<512>; EXPR; } break;  \
+#define CHK_DISPATCH(n, ...)                               \
+  switch (n) {                                             \
+    case 8:   { using O = Ops<8>;   __VA_ARGS__; } break;  \
+    case 16:  { using O = Ops<16>;  __VA_ARGS__; } break;  \
+    case 32:  { using O = Ops<32>;  __VA_ARGS__; } break;  \
+    case 64:  { using O = Ops<64>;  __VA_ARGS__; } break;  \
+    case 128: { using O = Ops<128>; __VA_ARGS__; } break;  \
+    case 256: { using O = Ops<256>; __VA_ARGS__; } break;  \
+    case 512: { using O = Ops<512>; __VA_ARGS__; } break;  \
     default: return fail(CHK_EUNSUPPORTED, "unsupported n " + std::to_string(n)); \
   }
 
@@ -525,7 +533,7 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PlanDev pl = plan_dev(plan);
   SolveCtl ctl{w.st, w.Rh, w.part, w.hist, maxblk_of(n), opts->max_iter, opts->tol,
-               opts->precond_residual_stopping ? 1 : 0, 0};
+               opts->precond_residual_stopping ? 1 : 0, 0, nullptr, 0};
   if (const char* dbg = getenv("CHK_DEBUG_FLAGS")) ctl.dbg = atoi(dbg);
   RState* hst_all = g_pinned.get((size_t)2 * B);
   RState* hst = hst_all;
@@ -594,6 +602,144 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
     int stt = hst[b].status;
     if (stt == ST_ACTIVE) stt = ST_NOT_CONVERGED;  // defensive; max_iter always decides
     if (status) status[b] = stt;
+    if (iterations) iterations[b] = hst[b].iters;
+    if (final_rel) final_rel[b] = hst[b].final_rel;
+    if (rhs_projected) rhs_projected[b] = hst[b].rhs_projected;
+  }
+  return CHK_OK;
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------------------------------
+// slab decomposition (one grid over several GPUs)
+// ----------------------------------------------------------------------------
+static int slab_geo(const chk_grid* grid, const chk_slab* sl, const double* lo, const double* hi, SlabGeo* out) {
+  if (!sl || sl->nranks < 1 || sl->rank < 0 || sl->rank >= sl->nranks)
+    return fail(CHK_EINVAL, "bad slab (nranks/rank)");
+  int ok = 0;
+  CHK_DISPATCH(grid->n, {
+    ok = O::slab_ok(sl->nranks);
+    if (ok) *out = O::slab(sl->nranks, sl->rank, lo, hi);
+  });
+  if (!ok) return fail(CHK_EINVAL, "nranks must divide n and the middle-pass tile count");
+  return CHK_OK;
+}
+
+struct SlabWs {
+  double2* Rh;
+  double* part;
+  RState* st;
+  double* hist;
+  size_t bytes;
+};
+
+static SlabWs slab_carve(void* base, int n, int P, int B, int max_iter) {
+  const size_t spec_loc = (size_t)n * n * (n / 2 + 1) / P;
+  char* c = static_cast<char*>(base);
+  SlabWs w{};
+  size_t off = 0;
+  w.Rh = reinterpret_cast<double2*>(c + off); off = align_up(off + sizeof(double2) * spec_loc * B);
+  w.part = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * 2 * (size_t)maxblk_of(n) * B);
+  w.st = reinterpret_cast<RState*>(c + off); off = align_up(off + sizeof(RState) * B);
+  w.hist = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * (size_t)max_iter * B);
+  w.bytes = off;
+  return w;
+}
+
+extern "C" {
+
+size_t chk_slab_exchange_elems(const chk_grid* grid, const chk_slab* slab, int32_t B) {
+  if (!grid || !slab || !supported_n(grid->n) || slab->nranks < 1 || B < 1) return 0;
+  const size_t n = grid->n;
+  return n * n * (n / 2 + 1) / slab->nranks * (size_t)B;
+}
+
+size_t chk_slab_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, const chk_slab* slab,
+                                int32_t B, int32_t max_iter) {
+  if (!grid || !plan || !slab || B < 1 || max_iter < 1 || !supported_n(grid->n) || slab->nranks < 1) return 0;
+  return slab_carve(nullptr, grid->n, slab->nranks, B, max_iter).bytes;
+}
+
+int32_t chk_slab_phase(const chk_grid* grid, const chk_precond_plan* plan, const chk_slab* slab,
+                       int32_t phase, int32_t it, const double* beta, const double* f, double* u, double* p,
+                       void* xa, void* xb, const double* halo_lo, const double* halo_hi, double* red,
+                       int32_t B, const chk_pcg_opts* opts, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  Geo g;
+  int rc = check_grid(grid, &g);
+  if (rc) return rc;
+  if (!plan || plan->n != grid->n || !opts || B < 1 || !red) return fail(CHK_EINVAL, "bad arguments");
+  SlabGeo sg;
+  if ((rc = slab_geo(grid, slab, halo_lo, halo_hi, &sg))) return rc;
+  const int n = grid->n;
+  SlabWs w = slab_carve(workspace, n, slab->nranks, B, opts->max_iter);
+  if (!workspace || workspace_bytes < w.bytes) return fail(CHK_EINVAL, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  PlanDev pl = plan_dev(plan);
+  SolveCtl ctl{w.st, w.Rh, w.part, w.hist, maxblk_of(n), opts->max_iter, opts->tol,
+               opts->precond_residual_stopping ? 1 : 0, 0, red, 1};
+  double2* XA = static_cast<double2*>(xa);
+  double2* XB = static_cast<double2*>(xb);
+  const double ntot = (double)n * n * n;
+  auto zero_red = [&]() { return cudaMemsetAsync(red, 0, sizeof(double) * 4 * B, s); };
+  auto decide = [&](int what) -> int {
+    decide_kernel<<<1, 256, 0, s>>>(ctl, red, B, what, it, ntot);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  };
+  CHK_DISPATCH(n, {
+    switch (phase) {
+      case CHK_SLAB_STATS:
+        CHK_CUDA(cudaMemsetAsync(w.st, 0, sizeof(RState) * B, s));
+        CHK_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(double) * (size_t)opts->max_iter * B, s));
+        CHK_CUDA(zero_red());
+        rc = O::rhs_stats(s, B, f, ctl, sg);
+        break;
+      case CHK_SLAB_STATS_DECIDE: rc = decide(DECIDE_STATS); break;
+      case CHK_SLAB_FWD_INIT: rc = O::fwd(FWD_INIT, s, B, g, beta, f, u, XA, pl, ctl, 0, sg); break;
+      case CHK_SLAB_MID:
+        CHK_CUDA(zero_red());
+        rc = O::mid(it == 0 ? MID_INIT : MID_ITER, s, B, XB, pl, ctl, it, sg);
+        break;
+      case CHK_SLAB_MID_DECIDE: rc = decide(DECIDE_MID); break;
+      case CHK_SLAB_INV: rc = O::inv(it == 0 ? INV_INIT : INV_ITER, s, B, XA, p, u, pl, ctl, it, sg); break;
+      case CHK_SLAB_FWD_Q:
+        CHK_CUDA(zero_red());
+        rc = O::fwd(FWD_Q, s, B, g, beta, p, u, XA, pl, ctl, it, sg);
+        break;
+      case CHK_SLAB_ALPHA_DECIDE: rc = decide(DECIDE_ALPHA); break;
+      case CHK_SLAB_MEANU:
+        CHK_CUDA(zero_red());
+        rc = O::mean_u(s, B, u, ctl, sg);
+        break;
+      case CHK_SLAB_MEANU_APPLY: {
+        if ((rc = decide(DECIDE_MEANU))) break;
+        const size_t nb = (size_t)sg.nloc * n * n;
+        sub_mean_kernel<<<1184, 256, 0, s>>>(u, w.st, nb, B);
+        CHK_LAUNCHED();
+        break;
+      }
+      default: return fail(CHK_EINVAL, "unknown slab phase");
+    }
+  });
+  return rc;
+}
+
+int32_t chk_slab_read_state(const chk_grid* grid, const chk_slab* slab, int32_t B, int32_t max_iter,
+                            void* workspace, int32_t* iterations, double* final_rel, int32_t* status,
+                            int32_t* rhs_projected, double* history, void* stream) {
+  if (!grid || !slab || !workspace || B < 1 || max_iter < 1 || !supported_n(grid->n))
+    return fail(CHK_EINVAL, "bad arguments");
+  SlabWs w = slab_carve(workspace, grid->n, slab->nranks, B, max_iter);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<RState> hst(B);
+  CHK_CUDA(cudaMemcpyAsync(hst.data(), w.st, sizeof(RState) * B, cudaMemcpyDeviceToHost, s));
+  if (history)
+    CHK_CUDA(cudaMemcpyAsync(history, w.hist, sizeof(double) * (size_t)max_iter * B, cudaMemcpyDeviceToHost, s));
+  CHK_CUDA(cudaStreamSynchronize(s));
+  for (int b = 0; b < B; ++b) {
+    if (status) status[b] = hst[b].status == ST_ACTIVE ? 3 : hst[b].status;
     if (iterations) iterations[b] = hst[b].iters;
     if (final_rel) final_rel[b] = hst[b].final_rel;
     if (rhs_projected) rhs_projected[b] = hst[b].rhs_projected;

@@ -56,6 +56,29 @@ struct Geo {
   double lam;
 };
 
+// Ownership of a rank when one grid is slab-decomposed over P GPUs (SURVEY
+// §8e): planes x0 in [x0_off, x0_off + nloc), spectral column chunk `rank`
+// (ncols = NR*(n/2+1)/P columns, tiles [tile_off, tile_off + tiles) of the
+// middle pass).  Exchange buffers are laid out [chunk s][b][x0 local][g][ncols]
+// so one all_to_all moves x0 slabs <-> column chunks.  P = 1 is the
+// single-GPU layout (nloc = n, one chunk, periodic halo inside p).
+struct SlabGeo {
+  int nloc;
+  int x0_off;
+  int P;
+  int ncols;
+  int tile_off;
+  int tiles;
+  const double* halo_lo;  // [B][n*n] plane x0_off-1, null -> periodic inside p
+  const double* halo_hi;  // [B][n*n] plane x0_off+nloc, null -> periodic inside p
+};
+
+// start of the (s, b, x0l, g) row chunk of an exchange buffer (complex units)
+__host__ __device__ __forceinline__ size_t slab_row(const SlabGeo& sg, int B, int G, int s, int b, int x0l,
+                                                    int g) {
+  return ((((size_t)s * B + b) * sg.nloc + x0l) * G + g) * (size_t)sg.ncols;
+}
+
 struct SolveCtl {
   RState* st;        // [B]
   double2* Rh;       // [B][TILES][N][G*W] residual spectrum, tile-major (PCG)
@@ -66,6 +89,8 @@ struct SolveCtl {
   double tol;
   int prs;           // precond_residual_stopping
   int dbg;           // timing experiments only (CHK_DEBUG_FLAGS), 0 in production
+  double* red;       // [B][4] rank-local sums (slab mode), null otherwise
+  int red_only;      // slab mode: last CTAs publish rank-local sums, decisions after allreduce
 };
 
 struct PlanDev {
@@ -168,17 +193,29 @@ struct RowCtx {
                          // {(x0-1,x1-1), (x0-1,x1), (x0,x1-1), (x0,x1)}; null = outside sub-cell
 };
 
-__device__ __forceinline__ RowCtx make_row(const double* __restrict__ p, const double* __restrict__ beta,
+// Base pointers of planes x0-1, x0, x0+1 of one realization (slab halos or
+// the periodic wrap inside p).
+struct Planes {
+  const double* m;
+  const double* c;
+  const double* p;
+};
+
+__device__ __forceinline__ Planes periodic_planes(const double* pb, int x0, int n) {
+  const size_t nn = (size_t)n * n;
+  return Planes{pb + (size_t)((x0 - 1) & (n - 1)) * nn, pb + (size_t)x0 * nn, pb + (size_t)((x0 + 1) & (n - 1)) * nn};
+}
+
+__device__ __forceinline__ RowCtx make_row(const Planes& pl, const double* __restrict__ beta,
                                            const Geo& g, int x0, int x1) {
   const int n = g.n, nm = n - 1;
-  const size_t nn = (size_t)n * n;
-  const int a0 = (x0 - 1) & nm, p0 = (x0 + 1) & nm, a1 = (x1 - 1) & nm, p1 = (x1 + 1) & nm;
+  const int a0 = (x0 - 1) & nm, a1 = (x1 - 1) & nm, p1 = (x1 + 1) & nm;
   RowCtx rc;
-  rc.pc = p + (size_t)x0 * nn + (size_t)x1 * n;
-  rc.pxm = p + (size_t)a0 * nn + (size_t)x1 * n;
-  rc.pxp = p + (size_t)p0 * nn + (size_t)x1 * n;
-  rc.pym = p + (size_t)x0 * nn + (size_t)a1 * n;
-  rc.pyp = p + (size_t)x0 * nn + (size_t)p1 * n;
+  rc.pc = pl.c + (size_t)x1 * n;
+  rc.pxm = pl.m + (size_t)x1 * n;
+  rc.pxp = pl.p + (size_t)x1 * n;
+  rc.pym = pl.c + (size_t)a1 * n;
+  rc.pyp = pl.c + (size_t)p1 * n;
   const int j0[2] = {a0, x0}, j1[2] = {a1, x1};
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -262,23 +299,20 @@ __device__ __forceinline__ void ldg4v(const double* p, double (&v)[4]) {
 }
 
 template <int N>
-__device__ __forceinline__ void stencil4_allin(const Geo& g, const double* __restrict__ p,
+__device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
                                                const double* __restrict__ beta, int x0, int x1,
                                                int x2s, double (&pc)[4], double (&q)[4]) {
   constexpr int nm = N - 1;
   constexpr int Q4 = N / 4;
   constexpr bool SHFL = (Q4 == 16 || Q4 == 32);
-  constexpr long long nn = (long long)N * N;
-  const long long row = (long long)x0 * nn + (long long)x1 * N;
-  const long long d0m = (x0 == 0) ? (long long)nm * nn : -nn;
-  const long long d0p = (x0 == nm) ? -(long long)nm * nn : nn;
+  const long long row = (long long)x1 * N;
   const long long d1m = (x1 == 0) ? (long long)nm * N : -(long long)N;
   const long long d1p = (x1 == nm) ? -(long long)nm * N : (long long)N;
-  const double* pr = p + row + x2s;
+  const double* pr = P3.c + row + x2s;
   double xm[4], xp[4], ym[4], yp[4];
   ldg4v(pr, pc);
-  ldg4v(pr + d0m, xm);
-  ldg4v(pr + d0p, xp);
+  ldg4v(P3.m + row + x2s, xm);
+  ldg4v(P3.p + row + x2s, xp);
   ldg4v(pr + d1m, ym);
   ldg4v(pr + d1p, yp);
   double pl, prr;
@@ -286,8 +320,8 @@ __device__ __forceinline__ void stencil4_allin(const Geo& g, const double* __res
     pl = __shfl_sync(0xffffffffu, pc[3], (threadIdx.x - 1) & (Q4 - 1), Q4);
     prr = __shfl_sync(0xffffffffu, pc[0], (threadIdx.x + 1) & (Q4 - 1), Q4);
   } else {
-    pl = __ldg(p + row + ((x2s - 1) & nm));
-    prr = __ldg(p + row + ((x2s + 4) & nm));
+    pl = __ldg(P3.c + row + ((x2s - 1) & nm));
+    prr = __ldg(P3.c + row + ((x2s + 4) & nm));
   }
   // cell rows (c(j0), c(j1), :) for j0 in {x0-1, x0}, j1 in {x1-1, x1}
   const int L = g.L, sh = g.sh;
@@ -325,13 +359,13 @@ __device__ __forceinline__ void stencil4_allin(const Geo& g, const double* __res
 }
 
 template <int N, bool ALLIN>
-__device__ __forceinline__ void stencil_quad(const Geo& g, const double* __restrict__ p,
+__device__ __forceinline__ void stencil_quad(const Geo& g, const Planes& P3,
                                              const double* __restrict__ beta, int x0, int x1,
                                              int x2s, double (&pc)[4], double (&q)[4]) {
   if constexpr (ALLIN) {
-    stencil4_allin<N>(g, p, beta, x0, x1, x2s, pc, q);
+    stencil4_allin<N>(g, P3, beta, x0, x1, x2s, pc, q);
   } else {
-    const RowCtx rc = make_row(p, beta, g, x0, x1);
+    const RowCtx rc = make_row(P3, beta, g, x0, x1);
     stencil4(g, rc, x2s, pc, q);
   }
 }
@@ -350,13 +384,14 @@ __global__ void __launch_bounds__(256) stencil_apply_kernel(Geo g, const double*
   const size_t nb = (size_t)N * N * N;
   const double* xb = x + b * nb;
   const double* bb = beta + (size_t)b * g.L * g.L * g.L;
+  const Planes P3 = periodic_planes(xb, x0, N);
   double acc = 0.0;
   constexpr int Q4 = N / 4;
   for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
     const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
     const int x1 = gg + G * t;
     double pc[4], q[4];
-    stencil_quad<N, ALLIN>(g, xb, bb, x0, x1, x2, pc, q);
+    stencil_quad<N, ALLIN>(g, P3, bb, x0, x1, x2, pc, q);
     double2* yo = reinterpret_cast<double2*>(y + b * nb + ((size_t)x0 * N + x1) * N + x2);
     yo[0] = make_double2(q[0], q[1]);
     yo[1] = make_double2(q[2], q[3]);
@@ -503,17 +538,20 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
                                                         const double* __restrict__ src,  // x (APPLY) / f (INIT) / p (Q)
                                                         double* __restrict__ u,
                                                         double2* __restrict__ S, PlanDev pl,
-                                                        SolveCtl ctl, int it) {
+                                                        SolveCtl ctl, SlabGeo sg, int B, int it) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
   constexpr int HP = H;
   extern __shared__ double2 buf[];
   __shared__ double scratch[32];
-  const int b = blockIdx.x / (N * G);
-  const int rem = blockIdx.x - b * (N * G);
-  const int x0 = rem / G, gg = rem - (rem / G) * G;
-  const size_t nb = (size_t)N * N * N;
+  const int nlg = sg.nloc * G;
+  const int b = blockIdx.x / nlg;
+  const int rem = blockIdx.x - b * nlg;
+  const int x0l = rem / G, gg = rem - (rem / G) * G;  // local plane, x1 group
+  const int x0 = sg.x0_off + x0l;                     // global plane
+  const size_t nn = (size_t)N * N;
+  const size_t nb = (size_t)sg.nloc * nn;             // local DOF per realization
   double* sm = reinterpret_cast<double*>(buf);
   RState* st = (MODE == FWD_APPLY) ? nullptr : ctl.st + b;
   constexpr int Q4 = N / 4;
@@ -521,14 +559,14 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
   if (MODE == FWD_APPLY) {
     for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
       const int t = i / N, x2 = i - (i / N) * N;
-      sm[t * 2 * HP + x2] = __ldg(src + b * nb + ((size_t)x0 * N + gg + G * t) * N + x2);
+      sm[t * 2 * HP + x2] = __ldg(src + b * nb + ((size_t)x0l * N + gg + G * t) * N + x2);
     }
   } else if (MODE == FWD_INIT) {
     const int status = st->status;
     const double shift = st->rhs_projected ? st->mean_f : 0.0;  // solver.py:139-143
     for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
       const int t = i / N, x2 = i - (i / N) * N;
-      const size_t idx = b * nb + ((size_t)x0 * N + gg + G * t) * N + x2;
+      const size_t idx = b * nb + ((size_t)x0l * N + gg + G * t) * N + x2;
       u[idx] = 0.0;
       sm[t * 2 * HP + x2] = __ldg(src + idx) - shift;
     }
@@ -537,26 +575,34 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
     if (st->status != ST_ACTIVE) return;
     const double* pb = src + b * nb;
     const double* bb = beta + (size_t)b * g.L * g.L * g.L;
+    Planes P3;
+    P3.c = pb + (size_t)x0l * nn;
+    P3.m = (x0l > 0) ? P3.c - nn : (sg.halo_lo ? sg.halo_lo + b * nn : pb + (size_t)(N - 1) * nn);
+    P3.p = (x0l < sg.nloc - 1) ? P3.c + nn : (sg.halo_hi ? sg.halo_hi + b * nn : pb);
     double acc = 0.0;
     for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
       const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
       double pc[4], q[4];
-      stencil_quad<N, ALLIN>(g, pb, bb, x0, gg + G * t, x2, pc, q);
+      stencil_quad<N, ALLIN>(g, P3, bb, x0, gg + G * t, x2, pc, q);
       double2* s2 = reinterpret_cast<double2*>(sm + t * 2 * HP + x2);
       s2[0] = make_double2(q[0], q[1]);
       s2[1] = make_double2(q[2], q[3]);
       acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
     }
     double t0, t1;
-    if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G,
+    if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, nlg,
                      scratch, t0, t1)) {
       if (threadIdx.x == 0) {
-        if ((!(t0 > 0.0) || !isfinite(t0)) && !ctl.dbg) {  // solver.py:164-165
-          st->status = ST_BREAKDOWN;
-          st->iters = it;
+        if (ctl.red_only) {
+          ctl.red[4 * b] = t0;  // rank-local p.Ap, decided after the allreduce
+        } else {
+          if ((!(t0 > 0.0) || !isfinite(t0)) && !ctl.dbg) {  // solver.py:164-165
+            st->status = ST_BREAKDOWN;
+            st->iters = it;
+          }
+          st->pq = t0;
+          st->alpha = st->rz[(it - 1) & 1] / t0;  // solver.py:166
         }
-        st->pq = t0;
-        st->alpha = st->rz[(it - 1) & 1] / t0;  // solver.py:166
       }
     }
   }
@@ -568,12 +614,14 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
   __syncthreads();
   // C2C along the x1 group (length NR)
   fft_smem<NR, false, H>(buf, ColAddr{HP}, pl.tw, N);
-  // the slab is contiguous in smem (HP == H) and in HBM: one bulk store
-  double2* dst = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
+  // the slab row is contiguous in smem (HP == H); it leaves in P column chunks
+  // (one bulk store each; a single chunk when the grid is not slab-decomposed)
   fence_proxy_async_smem();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    bulk_s2g(dst, buf, (uint32_t)(NR * H * sizeof(double2)));
+  if (threadIdx.x < sg.P) {
+    const int c = threadIdx.x;
+    bulk_s2g(S + slab_row(sg, B, G, c, b, x0l, gg), buf + (size_t)c * sg.ncols,
+             (uint32_t)(sg.ncols * sizeof(double2)));
     bulk_commit();
     bulk_wait_read0();
   }
@@ -601,6 +649,11 @@ __host__ __device__ __forceinline__ int mid_dsm_offset(int tile_elems, int gw, i
 // (rr = ||r||^2, rz = r.z, both already divided by N^3).
 __device__ __forceinline__ void mid_decide(RState* st, const SolveCtl& ctl, int b, int it, double rr,
                                            double rz) {
+  if (ctl.red_only) {  // slab mode: rank-local sums, decided after the allreduce
+    ctl.red[4 * b + 1] = rr;
+    ctl.red[4 * b + 2] = rz;
+    return;
+  }
   if (it == 0) {
     st->normf = sqrt(rr);  // solver.py:132 (after the optional projection, :142)
     if (!(rr > 0.0)) {     // projected RHS vanished (solver.py:144-148)
@@ -730,11 +783,12 @@ __device__ __forceinline__ double2 mid_point(double2 v, double D, double wgt, do
 // Shared-memory stage kernel (any n; used for n >= 256).
 template <int N, int G, int W, int NB, int MODE>
 __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S, PlanDev pl,
-                                                         SolveCtl ctl, int it, int B) {
+                                                         SolveCtl ctl, SlabGeo sg, int it, int B) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
-  constexpr int TILES = NR * H / W;
+  const int TILES = sg.tiles;  // tiles of this rank (all NR*H/W when not slab-decomposed)
+  const int nsh = __ffs(sg.nloc) - 1;  // nloc is a power of two
   constexpr int GW = G * W;
   constexpr int RS = GW + 1;
   extern __shared__ double2 buf[];  // [N][RS] data tile (aliased by the [r1][GW] coefficients)
@@ -748,7 +802,8 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
   __shared__ double s_alpha[NB];
   const int bg = blockIdx.x / TILES;
   const int tile = blockIdx.x - bg * TILES;
-  const int c0 = tile * W;
+  const int c0 = tile * W;                       // first column inside this rank's chunk
+  const int cg0 = (sg.tile_off + tile) * W;      // global spectral column
   const int b0 = bg * NB;
   if (threadIdx.x == 0) {
     int any = 0;
@@ -764,16 +819,15 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
   }
   __syncthreads();
   if (scratch[0] == 0.0) return;
-  mid_prologue<N, G, W, MODE>(buf, Dsm, c0, pl, s_k1, s_k2, s_wgt, s_tw);
+  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw);
 
   const double scale = 2.0 / ((double)N * N * N);
   for (int j = 0; j < NB; ++j) {
     if (!s_act[j]) continue;
     const int b = b0 + j;
-    double2* base = S + (size_t)b * N * G * (NR * H);
     for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
       const int w = i % W, gq = (i / W) % G, x0 = i / GW;
-      double2 v = base[((size_t)x0 * G + gq) * (NR * H) + c0 + w];
+      double2 v = S[slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), gq) + c0 + w];
       if (G > 1) v = cmul(v, s_tw[gq * W + w]);
       buf[x0 * RS + gq * W + w] = v;
     }
@@ -794,7 +848,7 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
       const int w = i % W, gq = (i / W) % G, x0 = i / GW;
       double2 v = buf[x0 * RS + gq * W + w];
       if (G > 1) v = cmulc(v, s_tw[gq * W + w]);
-      base[((size_t)x0 * G + gq) * (NR * H) + c0 + w] = v;
+      S[slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), gq) + c0 + w] = v;
     }
     if (MODE != MID_APPLY) {
       RState* st = ctl.st + b;
@@ -860,11 +914,12 @@ __device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restri
 // way).  P realizations are in flight per CTA; NB share one diagonal tile.
 template <int N, int G, int W, int RA, int NB, int P, int MODE, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* __restrict__ S, PlanDev pl,
-                                                                      SolveCtl ctl, int it, int B) {
+                                                                      SolveCtl ctl, SlabGeo sg, int it, int B) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
-  constexpr int TILES = NR * H / W;
+  const int TILES = sg.tiles;  // tiles of this rank (all NR*H/W when not slab-decomposed)
+  const int nsh = __ffs(sg.nloc) - 1;  // nloc is a power of two
   constexpr int GW = G * W;
   constexpr int RS = GW + 1;
   constexpr int RB = N / RA;      // positions per phase-B block
@@ -884,7 +939,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
   __shared__ double s_alpha[NB];
   const int bg = blockIdx.x / TILES;
   const int tile = blockIdx.x - bg * TILES;
-  const int c0 = tile * W;
+  const int c0 = tile * W;                       // first column inside this rank's chunk
+  const int cg0 = (sg.tile_off + tile) * W;      // global spectral column
   const int b0 = bg * NB;
 
   if (threadIdx.x == 0) {
@@ -901,7 +957,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
   }
   __syncthreads();
   if (scratch[0] == 0.0) return;
-  mid_prologue<N, G, W, MODE>(buf, Dsm, c0, pl, s_k1, s_k2, s_wgt, s_tw);
+  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw);
 
   const double scale = 2.0 / ((double)N * N * N);
   const int ntab = N;
@@ -911,7 +967,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
       for (int i = threadIdx.x; i < P * N * G; i += blockDim.x) {
         const int pr = i / (N * G), rr = i - pr * (N * G);
         if (s_act[(c + 1) * P + pr])
-          bulk_prefetch_l2(S + (size_t)(b0 + (c + 1) * P + pr) * N * G * (NR * H) + (size_t)rr * (NR * H) + c0,
+          bulk_prefetch_l2(S + slab_row(sg, B, G, (rr / G) >> nsh, b0 + (c + 1) * P + pr, (rr / G) & (sg.nloc - 1),
+                                        rr % G) + c0,
                            W * sizeof(double2));
       }
     }
@@ -920,12 +977,14 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
       const int pr = item / ITEMS_A, ia = item - pr * ITEMS_A;
       if (!s_act[c * P + pr]) continue;
       const int w = ia % W, j = ia / W;
-      const double2* base = S + (size_t)(b0 + c * P + pr) * N * G * (NR * H) + c0 + w;
+      const int bb = b0 + c * P + pr;
       double2 v[G][RA];
 #pragma unroll
-      for (int t = 0; t < RA; ++t)
+      for (int t = 0; t < RA; ++t) {
+        const int x0 = j + JA * t;
 #pragma unroll
-        for (int g = 0; g < G; ++g) v[g][t] = base[((size_t)(j + JA * t) * G + g) * (NR * H)];
+        for (int g = 0; g < G; ++g) v[g][t] = S[slab_row(sg, B, G, x0 >> nsh, bb, x0 & (sg.nloc - 1), g) + c0 + w];
+      }
       if constexpr (G > 1) {
 #pragma unroll
         for (int g = 1; g < G; ++g) {
@@ -1021,11 +1080,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
           for (int t = 0; t < RA; ++t) v[g][t] = cmulc(v[g][t], tg);
         }
       }
-      double2* base = S + (size_t)(b0 + c * P + pr) * N * G * (NR * H) + c0 + w;
+      const int bb = b0 + c * P + pr;
 #pragma unroll
-      for (int t = 0; t < RA; ++t)
+      for (int t = 0; t < RA; ++t) {
+        const int x0 = j + JA * t;
 #pragma unroll
-        for (int g = 0; g < G; ++g) base[((size_t)(j + JA * t) * G + g) * (NR * H)] = v[g][t];
+        for (int g = 0; g < G; ++g) S[slab_row(sg, B, G, x0 >> nsh, bb, x0 & (sg.nloc - 1), g) + c0 + w] = v[g][t];
+      }
     }
     // ---- per-realization Parseval reductions and decisions ----
     if (MODE != MID_APPLY) {
@@ -1069,17 +1130,18 @@ __device__ __forceinline__ void stv4(double* p, const double (&v)[4]) {
 template <int N, int G, int MODE>
 __global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restrict__ S,
                                                         double* __restrict__ out, double* __restrict__ u,
-                                                        PlanDev pl, SolveCtl ctl, int it) {
+                                                        PlanDev pl, SolveCtl ctl, SlabGeo sg, int B, int it) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
   constexpr int HP = H;
   extern __shared__ double2 buf[];
   __shared__ alignas(8) uint64_t bar;
-  const int b = blockIdx.x / (N * G);
-  const int rem = blockIdx.x - b * (N * G);
-  const int x0 = rem / G, gg = rem - (rem / G) * G;
-  const size_t nb = (size_t)N * N * N;
+  const int nlg = sg.nloc * G;
+  const int b = blockIdx.x / nlg;
+  const int rem = blockIdx.x - b * nlg;
+  const int x0 = rem / G, gg = rem - (rem / G) * G;  // local plane, x1 group
+  const size_t nb = (size_t)sg.nloc * N * N;
   double alpha = 0.0, beta = 0.0;
   bool do_p = true, do_u = false;
   if (MODE != INV_APPLY) {
@@ -1094,11 +1156,13 @@ __global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restric
     if (!do_p && !do_u) return;
   }
   if (do_p) {
-    const double2* srcp = S + ((size_t)(b * N + x0) * G + gg) * (NR * H);
+    // the slab row arrives as P column chunks (one bulk load each)
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
       mbar_arrive_expect_tx(&bar, (uint32_t)(NR * H * sizeof(double2)));
-      bulk_g2s(buf, srcp, (uint32_t)(NR * H * sizeof(double2)), &bar);
+      for (int c = 0; c < sg.P; ++c)
+        bulk_g2s(buf + (size_t)c * sg.ncols, S + slab_row(sg, B, G, c, b, x0, gg),
+                 (uint32_t)(sg.ncols * sizeof(double2)), &bar);
     }
   }
   if (MODE == INV_ITER && threadIdx.x < NR) {
@@ -1148,16 +1212,36 @@ __global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restric
 }
 
 // ----------------------------------------------------------------------------
-// init / finalize reductions
+// init / finalize reductions and the slab-mode decision kernels
 // ----------------------------------------------------------------------------
+// RHS statistics -> zero-RHS / mean-projection decisions (solver.py:131-148).
+__device__ __forceinline__ void stats_decide(RState* st, double sum, double sumsq, double ntot) {
+  const double normf = sqrt(sumsq);
+  st->iters = 0;
+  st->final_rel = 0.0;
+  st->rz[0] = st->rz[1] = 0.0;
+  st->beta = 0.0;
+  st->mean_u = 0.0;
+  if (!(normf > 0.0)) {  // zero right-hand side (solver.py:131-136)
+    st->status = ST_CONVERGED;
+    st->rhs_projected = 0;
+    st->mean_f = 0.0;
+  } else {
+    st->status = ST_ACTIVE;
+    st->rhs_projected = fabs(sum) > 1e-10 * normf ? 1 : 0;  // solver.py:139
+    st->mean_f = sum / ntot;
+  }
+}
+
 template <int N, int G>
-__global__ void __launch_bounds__(256) rhs_stats_kernel(const double* __restrict__ f, SolveCtl ctl) {
+__global__ void __launch_bounds__(256) rhs_stats_kernel(const double* __restrict__ f, SolveCtl ctl, SlabGeo sg) {
   constexpr int NR = N / G;
   __shared__ double scratch[32];
-  const int b = blockIdx.x / (N * G);
-  const int rem = blockIdx.x - b * (N * G);
+  const int nlg = sg.nloc * G;
+  const int b = blockIdx.x / nlg;
+  const int rem = blockIdx.x - b * nlg;
   const int x0 = rem / G, gg = rem - (rem / G) * G;
-  const size_t nb = (size_t)N * N * N;
+  const size_t nb = (size_t)sg.nloc * N * N;
   RState* st = ctl.st + b;
   double s = 0.0, s2 = 0.0;
   for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
@@ -1167,36 +1251,28 @@ __global__ void __launch_bounds__(256) rhs_stats_kernel(const double* __restrict
     s2 += v * v;
   }
   double t0, t1;
-  if (reduce2_last(s, s2, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G, scratch,
+  if (reduce2_last(s, s2, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, nlg, scratch,
                    t0, t1)) {
     if (threadIdx.x == 0) {
-      const double normf = sqrt(t1);
-      st->iters = 0;
-      st->final_rel = 0.0;
-      st->rz[0] = st->rz[1] = 0.0;
-      st->beta = 0.0;
-      st->mean_u = 0.0;
-      if (!(normf > 0.0)) {  // zero right-hand side (solver.py:131-136)
-        st->status = ST_CONVERGED;
-        st->rhs_projected = 0;
-        st->mean_f = 0.0;
+      if (ctl.red_only) {
+        ctl.red[4 * b] = t0;
+        ctl.red[4 * b + 1] = t1;
       } else {
-        st->status = ST_ACTIVE;
-        st->rhs_projected = fabs(t0) > 1e-10 * normf ? 1 : 0;  // solver.py:139
-        st->mean_f = t0 / (double)nb;
+        stats_decide(st, t0, t1, (double)N * N * N);
       }
     }
   }
 }
 
 template <int N, int G>
-__global__ void __launch_bounds__(256) mean_u_kernel(const double* __restrict__ u, SolveCtl ctl) {
+__global__ void __launch_bounds__(256) mean_u_kernel(const double* __restrict__ u, SolveCtl ctl, SlabGeo sg) {
   constexpr int NR = N / G;
   __shared__ double scratch[32];
-  const int b = blockIdx.x / (N * G);
-  const int rem = blockIdx.x - b * (N * G);
+  const int nlg = sg.nloc * G;
+  const int b = blockIdx.x / nlg;
+  const int rem = blockIdx.x - b * nlg;
   const int x0 = rem / G, gg = rem - (rem / G) * G;
-  const size_t nb = (size_t)N * N * N;
+  const size_t nb = (size_t)sg.nloc * N * N;
   RState* st = ctl.st + b;
   double s = 0.0;
   for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
@@ -1204,9 +1280,12 @@ __global__ void __launch_bounds__(256) mean_u_kernel(const double* __restrict__ 
     s += u[b * nb + ((size_t)x0 * N + gg + G * t) * N + x2];
   }
   double t0, t1;
-  if (reduce2_last(s, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, N * G, scratch,
+  if (reduce2_last(s, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, nlg, scratch,
                    t0, t1)) {
-    if (threadIdx.x == 0) st->mean_u = t0 / (double)nb;
+    if (threadIdx.x == 0) {
+      if (ctl.red_only) ctl.red[4 * b + 3] = t0;
+      else st->mean_u = t0 / ((double)N * N * N);
+    }
   }
 }
 
@@ -1217,6 +1296,36 @@ __global__ void __launch_bounds__(256) sub_mean_kernel(double* __restrict__ u, c
        i += (size_t)gridDim.x * blockDim.x) {
     const int b = (int)(i / nb);
     u[i] -= st[b].mean_u;  // solver.py:169 (applied once: proj is linear and idempotent)
+  }
+}
+
+// Slab mode: decisions from the allreduced sums red[B][4] (identical on every
+// rank, so every rank takes the same decisions).
+enum : int { DECIDE_STATS = 0, DECIDE_ALPHA = 1, DECIDE_MID = 2, DECIDE_MEANU = 3 };
+
+__global__ void decide_kernel(SolveCtl ctl, const double* __restrict__ red, int B, int what, int it,
+                              double ntot) {
+  SolveCtl c = ctl;
+  c.red_only = 0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    RState* st = ctl.st + b;
+    if (what == DECIDE_STATS) {
+      stats_decide(st, red[4 * b], red[4 * b + 1], ntot);
+    } else if (what == DECIDE_MEANU) {
+      st->mean_u = red[4 * b + 3] / ntot;
+    } else if (st->status == ST_ACTIVE) {
+      if (what == DECIDE_ALPHA) {
+        const double pq = red[4 * b];
+        if ((!(pq > 0.0) || !isfinite(pq)) && !ctl.dbg) {  // solver.py:164-165
+          st->status = ST_BREAKDOWN;
+          st->iters = it;
+        }
+        st->pq = pq;
+        st->alpha = st->rz[(it - 1) & 1] / pq;  // solver.py:166
+      } else {
+        mid_decide(st, c, b, it, red[4 * b + 1], red[4 * b + 2]);  // already / N^3
+      }
+    }
   }
 }
 

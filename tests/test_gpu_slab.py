@@ -1,0 +1,83 @@
+"""Slab-decomposed PCG on one GPU: P virtual ranks run the exact
+multi-GPU schedule (LocalComm) and must reproduce the single-GPU batched solver
+and the reference's golden run of config 5 (n = 512)."""
+
+import numpy as np
+import pytest
+
+from oracle import checkerhom_oracle as orc
+
+from conftest import golden_configs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+import paper_2007_06524_b200 as chk  # noqa: E402
+from paper_2007_06524_b200 import slab  # noqa: E402
+
+
+def _problem(cfg_id, ms):
+    c = orc.CONFIGS[cfg_id]
+    cfg = chk.LatticeConfig(d=3, L=c["L"], n0=c["n0"], alpha="1/2", lam=c["lam"])
+    rs = [chk.sample_realization(cfg, chk.derive_seed(0, m)) for m in ms]
+    beta = np.stack([r.beta_cells.ravel() for r in rs])
+    A = chk.StiffnessBatch(cfg, beta)
+    if c["rhs"] == "corrector":
+        F = chk.corrector_rhs_batched(A, 1)
+    else:
+        F = torch.stack([torch.as_tensor(orc.gaussian_rhs(cfg.n, r.seed)) for r in rs]).cuda()
+    opts = chk.SolveOptions(tol=c["tol"], preconditioner="lkr", eps_rank=1e-8)
+    return cfg, beta, A, F, opts
+
+
+def _slab(cfg, beta, F, opts, P):
+    n = cfg.n
+    nloc = n // P
+    Fv = F.reshape(F.shape[0], n, n * n)
+    ranks = [slab.SlabRank(cfg, beta, Fv[:, r * nloc:(r + 1) * nloc].contiguous(), P, r, opts)
+             for r in range(P)]
+    res = slab.slab_solve(ranks, slab.LocalComm(P))
+    u = torch.cat([x.reshape(F.shape[0], nloc, n * n) for x in res.u], dim=1).reshape(F.shape[0], -1)
+    return res, u
+
+
+@pytest.mark.parametrize("cfg_id,ms,P", [(2, [0, 1, 2], 2), (2, [3], 4), (3, [0, 1], 8), (4, [0], 2)])
+def test_slab_matches_single_gpu(cfg_id, ms, P):
+    cfg, beta, A, F, opts = _problem(cfg_id, ms)
+    ref = chk.pcg_solve_batched(A, F, opts)
+    res, u = _slab(cfg, beta, F, opts, P)
+    assert list(res.iterations) == list(ref.iterations)
+    assert np.all(res.status == 0)
+    for j in range(len(ms)):
+        its = int(ref.iterations[j])
+        assert np.allclose(res.history[j, :its], ref.history[j, :its], rtol=1e-9, atol=0)
+        rel = float(torch.linalg.norm(u[j] - ref.u[j]) / torch.linalg.norm(ref.u[j]))
+        assert rel <= 1e-10, rel
+
+
+def test_slab_config5_n512_vs_reference():
+    """n = 512 slab-decomposed over 2 ranks: the reference's iteration count
+    and solution probes (config 5, golden from the reference run)."""
+    recs = golden_configs(5)
+    if not recs:
+        pytest.skip("config 5 golden not generated")
+    rec = recs[0]
+    cfg, beta, A, F, opts = _problem(5, [0])
+    res, u = _slab(cfg, beta, F, opts, 2)
+    assert int(res.iterations[0]) == rec["iterations"]
+    its = rec["iterations"]
+    assert np.allclose(res.history[0, :its], rec["residuals"], rtol=1e-7, atol=0)
+    uu = u[0].cpu().numpy()
+    assert abs(np.linalg.norm(uu) - rec["norm_u"]) <= 1e-9 * rec["norm_u"]
+    idx = np.random.default_rng(rec["probe_idx_seed"]).integers(0, uu.size, size=len(rec["u_probe"]))
+    probe = np.asarray(rec["u_probe"])
+    assert np.max(np.abs(uu[idx] - probe)) <= 1e-8 * np.max(np.abs(probe))
+
+
+def test_slab_rejects_bad_geometry():
+    cfg, beta, A, F, opts = _problem(2, [0])
+    with pytest.raises(ValueError):
+        slab.SlabRank(cfg, beta, F, 3, 0, opts)  # 3 does not divide n = 64
