@@ -396,6 +396,99 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_slab(args):
+    """Config 5 on N > 1 GPUs: one n = 512 grid slab-decomposed over the ranks
+    (strong scaling; NCCL halo exchange, all_to_all transposes, allreduces)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2007_06524_b200 as chk
+    from paper_2007_06524_b200 import slab
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world == 1 and "MASTER_ADDR" not in os.environ:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29517", RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    c = CFG[args.config]
+    lat = chk.LatticeConfig(d=3, L=c["L"], n0=c["n0"], alpha="1/2", lam=c["lam"])
+    n, nloc = lat.n, lat.n // world
+    beta = np.stack([chk.sample_realization(lat, chk.derive_seed(0, m)).beta_cells.ravel()
+                     for m in range(c["batch"])])
+    A = chk.StiffnessBatch(lat, beta)
+    F = chk.corrector_rhs_batched(A, 1)  # full field on every rank, local planes kept
+    Floc = F.reshape(c["batch"], n, n * n)[:, rank * nloc:(rank + 1) * nloc].contiguous()
+    del F, A
+    opts = chk.SolveOptions(tol=c["tol"], preconditioner="lkr", eps_rank=1e-8)
+    R = slab.SlabRank(lat, beta, Floc, world, rank, opts, device=dev)
+    comm = slab.TorchComm()
+
+    def step():
+        return slab.slab_solve([R], comm)
+
+    for _ in range(args.warmup):
+        res = step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    dof_its = 0
+    for _ in range(args.steps):
+        res = step()
+        dof_its += int(np.sum(res.iterations)) * n ** 3
+    e1.record()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    # e2e: host buffers of this rank's planes in, u out
+    f_h = Floc.cpu().pin_memory()
+    u_h = torch.empty_like(f_h).pin_memory()
+    e2e = []
+    for k in range(args.warmup + args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        R.f.copy_(f_h.reshape(R.f.shape), non_blocking=True)
+        res = step()
+        u_h.copy_(res.u[0].reshape(u_h.shape), non_blocking=True)
+        t1.record()
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            e2e.append(t0.elapsed_time(t1))
+    e2e_ms = torch.tensor([float(np.mean(e2e))], dtype=torch.float64, device=dev)
+    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        value = dof_its / (float(ms) / 1e3)
+        per_step = int(np.sum(res.iterations)) * n ** 3
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(ms) / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference seeded generator)",
+            "config": {"workload": f"config{args.config}: {CONFIG_NAMES[args.config]}", "n": n,
+                       "parallelism": f"slab x{world} (x0 planes; NCCL halo + all_to_all + allreduce)"},
+            "realizations_per_s": c["batch"] * args.steps / (float(ms) / 1e3),
+            "roofline": {"bound": "hbm", "kernel": "whole iteration", "unit": "GB/s", "peak": peak * world,
+                         "peak_kind": peak_kind, "achieved": round(value * B_ALG / 1e9, 1),
+                         "frac": round(value * B_ALG / 1e9 / (peak * world), 3), "traffic": None},
+            "e2e": {"value": per_step / (float(e2e_ms) / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(f_h.numel() * 8) * world,
+                    "d2h_bytes_per_step": int(u_h.numel() * 8) * world, "ms_per_step": float(e2e_ms)},
+            "gpu_launches": None, "clocks": clk, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -404,9 +497,13 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=sorted(CFG))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true",
+                    help="force the slab-decomposed path (default for config 5 when N > 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.slab or (args.config == 5 and int(os.environ.get("WORLD_SIZE", "1")) > 1):
+        run_slab(args)
     else:
         run_ours(args)
 
