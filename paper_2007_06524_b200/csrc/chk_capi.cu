@@ -99,13 +99,16 @@ int fail(int code, const std::string& msg) {
 template <int N>
 struct Cfg;
 // NB realizations share one evaluation of the diagonal tile in the middle pass.
+#ifndef CHK_W128
+#define CHK_W128 16
+#endif
 // REG: register-resident middle pass (first x0 radix RA in phase A, P
 // realizations in flight per CTA); otherwise the shared-memory stage kernel.
 template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8,  NB = 4, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 16, REG = 1, RA = 8, P = 1; };
-template <> struct Cfg<128> { static constexpr int G = 2,  W = 8,  NB = 16, REG = 1, RA = 8, P = 1; };
+template <> struct Cfg<128> { static constexpr int G = 2,  W = CHK_W128, NB = 16, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 4, REG = 0, RA = 1, P = 1; };
 template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2, REG = 0, RA = 1, P = 1; };
 
@@ -165,7 +168,7 @@ struct Ops {
     dim3 grid(((B + NBX - 1) / NBX) * sg.tiles), block(256);
     if constexpr (REG) {
       constexpr int PX = (NBX == 1) ? 1 : P;
-      constexpr int NT = 128 * PX;
+      constexpr int NT = (W * (N / RA) > 128 ? 256 : 128) * PX;
       const size_t sm = (size_t)mid_dsm_offset(PX * N * (G * W + 1), G * W, r1) + (size_t)N * G * W * sizeof(double);
       CHK_CUDA(allow_smem(mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT>, sm));
       mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT><<<grid, NT, sm, s>>>(S, pl, ctl, sg, it, B);
@@ -463,6 +466,7 @@ int32_t chk_precond_apply(const chk_precond_plan* p, const double* r, double* z,
   double2* S = static_cast<double2*>(workspace);
   PlanDev pl = plan_dev(p);
   SolveCtl ctl{};
+  if (const char* dbg = getenv("CHK_DEBUG_FLAGS")) ctl.dbg = atoi(dbg);
   Geo g{};
   g.n = p->n;
   int rc = CHK_OK;

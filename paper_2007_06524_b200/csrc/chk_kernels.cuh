@@ -696,7 +696,7 @@ __device__ __forceinline__ void mid_decide(RState* st, const SolveCtl& ctl, int 
 // Shared prologue of both middle kernels: slot bookkeeping and the diagonal tile.
 template <int N, int G, int W, int MODE>
 __device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, const PlanDev& pl,
-                                             int* s_k1, int* s_k2, double* s_wgt, double2* s_tw) {
+                                             int* s_k1, int* s_k2, double* s_wgt, double2* s_tw, int dbg = 0) {
   constexpr int NR = N / G, N2 = N / 2, H = N2 + 1, GW = G * W;
   for (int s = threadIdx.x; s < GW; s += blockDim.x) {
     const int m = dig_freq<G>(s / W), w = s % W;
@@ -710,6 +710,7 @@ __device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, 
     s_tw[s] = __ldg(pl.tw + (s / W) * kp);  // as a load slot (group s/W, column w)
   }
   __syncthreads();
+  if (dbg & 16) return;  // timing experiment: no diagonal tile
   if (pl.kind == KIND_LKR) {
     // D = U0p^T C, C[r][slot] = U1[r][k1] U2[r][k2]: rank-r1 contraction, once per CTA
     double* coef = reinterpret_cast<double*>(buf);
@@ -720,25 +721,34 @@ __device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, 
       coef[rr * GW + s] = __ldg(U1 + rr * N + s_k1[s]) * __ldg(U2 + rr * N + s_k2[s]);
     }
     __syncthreads();
-    constexpr int PQ = N / 4, SQ = GW / 2;
+    // 4 positions x 4 slots per thread: 2 x 256-bit U0p loads + 2 smem loads per 16 FMA
+    constexpr int PQ = N / 4, SQ = GW / 4;
+    static_assert(GW % 4 == 0, "slots per tile must be a multiple of 4");
     for (int i = threadIdx.x; i < PQ * SQ; i += blockDim.x) {
       const int sq = i % SQ, pq = i / SQ;
-      double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
       const double* up = pl.Up + 4 * pq;
+      const double* cp = coef + 4 * sq;
+#pragma unroll 2
       for (int rr = 0; rr < pl.r1; ++rr) {
-        const double2 ua = __ldg(reinterpret_cast<const double2*>(up + (size_t)rr * N));
-        const double2 ub = __ldg(reinterpret_cast<const double2*>(up + (size_t)rr * N) + 1);
-        const double2 cc = *reinterpret_cast<const double2*>(coef + rr * GW + 2 * sq);
-        acc[0][0] = fma(ua.x, cc.x, acc[0][0]); acc[0][1] = fma(ua.x, cc.y, acc[0][1]);
-        acc[1][0] = fma(ua.y, cc.x, acc[1][0]); acc[1][1] = fma(ua.y, cc.y, acc[1][1]);
-        acc[2][0] = fma(ub.x, cc.x, acc[2][0]); acc[2][1] = fma(ub.x, cc.y, acc[2][1]);
-        acc[3][0] = fma(ub.y, cc.x, acc[3][0]); acc[3][1] = fma(ub.y, cc.y, acc[3][1]);
+        double u4[4];
+        ldg4v(up + (size_t)rr * N, u4);
+        const double2 c01 = *reinterpret_cast<const double2*>(cp + rr * GW);
+        const double2 c23 = *reinterpret_cast<const double2*>(cp + rr * GW + 2);
+        const double cc[4] = {c01.x, c01.y, c23.x, c23.y};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fma(u4[a], cc[c], acc[a][c]);
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        Dsm[(4 * pq + a) * GW + 2 * sq] = acc[a][0];
-        Dsm[(4 * pq + a) * GW + 2 * sq + 1] = acc[a][1];
-      }
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Dsm[(4 * pq + a) * GW + 4 * sq + c] = acc[a][c];
     }
   } else {
     for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
@@ -819,7 +829,7 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
   }
   __syncthreads();
   if (scratch[0] == 0.0) return;
-  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw);
+  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
 
   const double scale = 2.0 / ((double)N * N * N);
   for (int j = 0; j < NB; ++j) {
@@ -957,7 +967,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
   }
   __syncthreads();
   if (scratch[0] == 0.0) return;
-  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw);
+  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
 
   const double scale = 2.0 / ((double)N * N * N);
   const int ntab = N;
@@ -979,11 +989,19 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
       const int w = ia % W, j = ia / W;
       const int bb = b0 + c * P + pr;
       double2 v[G][RA];
+      if (sg.P == 1) {  // single chunk: rows are linear in x0
+        const double2* base = S + ((size_t)bb * N + j) * G * (size_t)sg.ncols + c0 + w;
 #pragma unroll
-      for (int t = 0; t < RA; ++t) {
-        const int x0 = j + JA * t;
+        for (int t = 0; t < RA; ++t)
 #pragma unroll
-        for (int g = 0; g < G; ++g) v[g][t] = S[slab_row(sg, B, G, x0 >> nsh, bb, x0 & (sg.nloc - 1), g) + c0 + w];
+          for (int g = 0; g < G; ++g) v[g][t] = base[(size_t)(JA * t * G + g) * sg.ncols];
+      } else {
+#pragma unroll
+        for (int t = 0; t < RA; ++t) {
+          const int x0 = j + JA * t;
+#pragma unroll
+          for (int g = 0; g < G; ++g) v[g][t] = S[slab_row(sg, B, G, x0 >> nsh, bb, x0 & (sg.nloc - 1), g) + c0 + w];
+        }
       }
       if constexpr (G > 1) {
 #pragma unroll
@@ -1003,6 +1021,17 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
         }
       }
       double2* dst = buf + pr * N * RS;
+      if (ctl.dbg & 32) {  // timing experiment: registers straight back out
+        const int bb2 = b0 + c * P + pr;
+#pragma unroll
+        for (int t = 0; t < RA; ++t)
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int x0 = j + JA * t;
+            S[slab_row(sg, B, G, x0 >> nsh, bb2, x0 & (sg.nloc - 1), g) + c0 + w] = v[g][t];
+          }
+        continue;
+      }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         dftR<RA, false>(v[g]);
@@ -1027,6 +1056,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
       double2 v[RB];
 #pragma unroll
       for (int e = 0; e < RB; ++e) v[e] = row[e * RS];
+      if (ctl.dbg & 8) continue;  // timing experiment: no phase-B work
       reg_fft<RB, false>(v, pl.tw, ntab);
       double rr = 0.0, rz = 0.0;
       const double wgt = s_wgt[s];
@@ -1081,11 +1111,19 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
         }
       }
       const int bb = b0 + c * P + pr;
+      if (sg.P == 1) {
+        double2* base = S + ((size_t)bb * N + j) * G * (size_t)sg.ncols + c0 + w;
 #pragma unroll
-      for (int t = 0; t < RA; ++t) {
-        const int x0 = j + JA * t;
+        for (int t = 0; t < RA; ++t)
 #pragma unroll
-        for (int g = 0; g < G; ++g) S[slab_row(sg, B, G, x0 >> nsh, bb, x0 & (sg.nloc - 1), g) + c0 + w] = v[g][t];
+          for (int g = 0; g < G; ++g) base[(size_t)(JA * t * G + g) * sg.ncols] = v[g][t];
+      } else {
+#pragma unroll
+        for (int t = 0; t < RA; ++t) {
+          const int x0 = j + JA * t;
+#pragma unroll
+          for (int g = 0; g < G; ++g) S[slab_row(sg, B, G, x0 >> nsh, bb, x0 & (sg.nloc - 1), g) + c0 + w] = v[g][t];
+        }
       }
     }
     // ---- per-realization Parseval reductions and decisions ----
