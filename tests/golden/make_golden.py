@@ -165,6 +165,23 @@ def small():
         out[pre + "name"] = np.array(rep.preconditioner)
         print("pcg", pi, rep.iterations, rep.converged, rep.preconditioner, flush=True)
 
+    # homogenized matrices (homogenize.py:92-124), d = 3
+    homog = [
+        dict(L=2, n0=4, alpha="1/4", lam=0.4, seed=11, tol=1e-8),
+        dict(L=4, n0=4, alpha="1/2", lam=0.1, seed=12, tol=1e-8),
+        dict(L=4, n0=4, alpha="1/4", lam=0.2, seed=13, tol=1e-9),
+    ]
+    for hi, kw in enumerate(homog):
+        cfg = ch.LatticeConfig(d=3, L=kw["L"], n0=kw["n0"], alpha=kw["alpha"], lam=kw["lam"])
+        r = ch.sample_realization(cfg, kw["seed"])
+        rec = ch.homogenized_matrix(r, ch.SolveOptions(tol=kw["tol"], preconditioner="lkr"))
+        pre = f"homog{hi}_"
+        out[pre + "meta"] = np.array([cfg.L, cfg.n0, cfg.k, cfg.offset, kw["seed"]], dtype=np.int64)
+        out[pre + "lam_tol"] = np.array([cfg.lam, kw["tol"]])
+        out[pre + "matrix"] = rec.matrix
+        out[pre + "its"] = np.array(rec.iterations)
+        print("homog", hi, rec.iterations, flush=True)
+
     # config 1 (n=32): full u for m = 0, 1
     for m in (0, 1):
         rec, u, f = config_run(1, m)

@@ -254,3 +254,32 @@ def test_size_mismatch_raises_value_error():
     cfg = chk.LatticeConfig(d=3, L=3, n0=4, lam=0.4)  # n = 12: not a power of two
     with pytest.raises(ValueError):
         chk.pcg_solve(chk.assemble_stiffness(chk.sample_realization(cfg, 1)), np.ones(12 ** 3))
+
+
+@pytest.mark.parametrize("hid", _case_ids("homog"))
+def test_homogenized_matrix_vs_reference(hid):
+    """homogenize.py:92-124 on the GPU: the three corrector solves batched,
+    <f_j, u_i> on the device; the reference's matrices and iteration counts."""
+    g = golden_small()
+    L, n0, k, off, seed = (int(v) for v in g[hid + "_meta"])
+    lam, tol = (float(v) for v in g[hid + "_lam_tol"])
+    cfg = chk.LatticeConfig(d=3, L=L, n0=n0, alpha=f"{k}/{2 * n0}", lam=lam, subcell_offset=off)
+    r = chk.sample_realization(cfg, seed)
+    rec = chk.homogenized_matrix(r, chk.SolveOptions(tol=tol, preconditioner="lkr"))
+    assert rec.iterations == tuple(int(v) for v in g[hid + "_its"])
+    ref = g[hid + "_matrix"]
+    assert np.max(np.abs(rec.matrix - ref)) <= 1e-9 * np.max(np.abs(ref))
+
+
+def test_ensemble_run_small():
+    cfg = chk.LatticeConfig(d=3, L=4, n0=4, alpha="1/2", lam=0.1)
+    stats = chk.ensemble_run(cfg, 6, 3, chk.SolveOptions(tol=1e-8, preconditioner="lkr"), chunk=4)
+    assert stats.M == 6 and stats.average.shape == (3, 3)
+    # symmetric homogenized matrices, positive diagonal below the arithmetic mean (Voigt bound)
+    for rec in stats.records:
+        assert np.max(np.abs(rec.matrix - rec.matrix.T)) <= 1e-6
+        assert np.all(np.diag(rec.matrix) > cfg.lam)
+    # realization order does not matter: same records as individual solves
+    r2 = chk.sample_realization(cfg, chk.derive_seed(3, 2))
+    one = chk.homogenized_matrix(r2, chk.SolveOptions(tol=1e-8, preconditioner="lkr"))
+    assert np.allclose(one.matrix, stats.records[2].matrix, rtol=1e-12, atol=1e-14)
