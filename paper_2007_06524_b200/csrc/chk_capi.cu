@@ -174,8 +174,8 @@ struct Ops {
       mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT><<<grid, NT, sm, s>>>(S, pl, ctl, sg, it, B);
     } else {
       const size_t sm = mid_smem(r1);
-      CHK_CUDA(allow_smem(mid_column_kernel<N, G, W, NBX, MODE>, sm));
-      mid_column_kernel<N, G, W, NBX, MODE><<<grid, block, sm, s>>>(S, pl, ctl, sg, it, B);
+      CHK_CUDA(allow_smem(mid_column_fused_kernel<N, G, W, NBX, MODE>, sm));
+      mid_column_fused_kernel<N, G, W, NBX, MODE><<<grid, block, sm, s>>>(S, pl, ctl, sg, it, B);
     }
     return CHK_OK;
   }

@@ -140,6 +140,39 @@ struct FftRec {
   }
 };
 
+// All stages but the last one (the last stage is the M == R stage: contiguous
+// groups of R, no twiddles), so a caller can fuse it with pointwise work.
+template <int N, int M, bool INV, int NP>
+struct FftRecButLast {
+  template <class Addr>
+  __device__ __forceinline__ static void run(double2* buf, const Addr& addr,
+                                             const double2* __restrict__ tw, int twstride) {
+    constexpr int R = Radix<M>::value;
+    if constexpr (M / R > 1) {
+      if constexpr (!INV) {
+        fft_stage<N, M, false, NP>(buf, addr, tw, twstride);
+        __syncthreads();
+        FftRecButLast<N, M / R, false, NP>::run(buf, addr, tw, twstride);
+      } else {
+        FftRecButLast<N, M / R, true, NP>::run(buf, addr, tw, twstride);
+        fft_stage<N, M, true, NP>(buf, addr, tw, twstride);
+        __syncthreads();
+      }
+    }
+  }
+};
+
+// radix of the last stage of fft_smem<N>
+template <int M>
+struct LastRadix {
+  static constexpr int R = Radix<M>::value;
+  static constexpr int value = (M / R > 1) ? LastRadix<M / R>::value : R;
+};
+template <>
+struct LastRadix<1> {
+  static constexpr int value = 1;
+};
+
 // Full length-N transform; the caller must __syncthreads() before (data in
 // smem); returns after a __syncthreads().  Forward: natural -> digit-reversed.
 // Inverse (unnormalised): digit-reversed -> natural, result scaled by N.

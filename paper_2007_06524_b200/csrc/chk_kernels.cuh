@@ -790,6 +790,157 @@ __device__ __forceinline__ double2 mid_point(double2 v, double D, double wgt, do
   return cscale(R, D * scale);
 }
 
+// In-register in-place DIF / inverse DIT of length L on v[0..L): identical
+// index semantics to fft_smem<L> (digit-reversed output), all loops unrolled.
+template <int L, int M, bool INV>
+struct RegFft {
+  __device__ __forceinline__ static void run(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
+    constexpr int R = Radix<M>::value, S = M / R;
+    if constexpr (INV && S > 1) RegFft<L, S, true>::run(v, tw, ntab);
+#pragma unroll
+    for (int blk = 0; blk < L / M; ++blk) {
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        double2 a[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) a[t] = v[blk * M + j + t * S];
+        if constexpr (!INV) {
+          dftR<R, false>(a);
+          if (j > 0) {
+#pragma unroll
+            for (int m = 1; m < R; ++m) a[m] = cmul(a[m], __ldg(tw + (j * m) * (ntab / M)));
+          }
+        } else {
+          if (j > 0) {
+#pragma unroll
+            for (int m = 1; m < R; ++m) a[m] = cmulc(a[m], __ldg(tw + (j * m) * (ntab / M)));
+          }
+          dftR<R, true>(a);
+        }
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[blk * M + j + t * S] = a[t];
+      }
+    }
+    if constexpr (!INV && S > 1) RegFft<L, S, false>::run(v, tw, ntab);
+  }
+};
+template <int L, bool INV>
+__device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
+  if constexpr (L > 1) RegFft<L, L, INV>::run(v, tw, ntab);
+}
+
+// Fused shared-memory kernel for large n (n >= 256: the plane slab forces G >= 8):
+// load + group combine in registers, the x0 stages but the last through shared
+// memory, [last forward stage + residual update + scaling + Parseval + first
+// inverse stage] in registers, remaining inverse stages, inverse group combine
+// + store in registers: 12 shared-memory passes per element instead of 20.
+template <int N, int G, int W, int NB, int MODE>
+__global__ void __launch_bounds__(256) mid_column_fused_kernel(double2* __restrict__ S, PlanDev pl,
+                                                               SolveCtl ctl, SlabGeo sg, int it, int B) {
+  constexpr int NR = N / G;
+  constexpr int N2 = N / 2;
+  constexpr int H = N2 + 1;
+  constexpr int GW = G * W;
+  constexpr int RS = GW + 1;
+  constexpr int RL = LastRadix<N>::value;  // radix of the fused last x0 stage
+  const int TILES = sg.tiles;
+  const int nsh = __ffs(sg.nloc) - 1;
+  extern __shared__ double2 buf[];
+  const int doff = mid_dsm_offset(N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
+  double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
+  __shared__ double scratch[32];
+  __shared__ int s_k1[GW], s_k2[GW];
+  __shared__ double s_wgt[GW];
+  __shared__ double2 s_tw[GW];
+  __shared__ int s_act[NB];
+  __shared__ double s_alpha[NB];
+  const int bg = blockIdx.x / TILES;
+  const int tile = blockIdx.x - bg * TILES;
+  const int c0 = tile * W;
+  const int cg0 = (sg.tile_off + tile) * W;
+  const int b0 = bg * NB;
+  if (threadIdx.x == 0) {
+    int any = 0;
+    for (int j = 0; j < NB; ++j) {
+      const int b = b0 + j;
+      int a = (b < B);
+      if (a && MODE != MID_APPLY) a = (ctl.st[b].status == ST_ACTIVE);
+      s_act[j] = a;
+      s_alpha[j] = (a && MODE == MID_ITER) ? ctl.st[b].alpha : 0.0;
+      any |= a;
+    }
+    scratch[0] = any;
+  }
+  __syncthreads();
+  if (scratch[0] == 0.0) return;
+  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
+  const double scale = 2.0 / ((double)N * N * N);
+  for (int j = 0; j < NB; ++j) {
+    if (!s_act[j]) continue;
+    const int b = b0 + j;
+    // ---- load + group combine (registers) -> smem ----
+    for (int item = threadIdx.x; item < N * W; item += blockDim.x) {
+      const int w = item % W, x0 = item / W;
+      const size_t rbase = slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), 0) + c0 + w;
+      double2 v[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) v[g] = S[rbase + (size_t)g * sg.ncols];
+#pragma unroll
+      for (int g = 1; g < G; ++g) v[g] = cmul(v[g], s_tw[g * W + w]);
+      reg_fft<G, false>(v, pl.tw, N);
+#pragma unroll
+      for (int g = 0; g < G; ++g) buf[x0 * RS + g * W + w] = v[g];
+    }
+    __syncthreads();
+    FftRecButLast<N, N, false, GW>::run(buf, X0Addr{RS}, pl.tw, 1);
+    // ---- last stage + residual / scaling + first inverse stage (registers) ----
+    double rr = 0.0, rz = 0.0;
+    double2* Rt = ctl.Rh + ((size_t)b * TILES + tile) * N * GW;
+    for (int item = threadIdx.x; item < GW * (N / RL); item += blockDim.x) {
+      const int s = item % GW, blk = item / GW;
+      double2 v[RL];
+#pragma unroll
+      for (int e = 0; e < RL; ++e) v[e] = buf[(blk * RL + e) * RS + s];
+      dftR<RL, false>(v);
+#pragma unroll
+      for (int e = 0; e < RL; ++e) {
+        const int pos0 = blk * RL + e;
+        v[e] = mid_point<MODE>(v[e], Dsm[pos0 * GW + s], s_wgt[s], scale, s_alpha[j],
+                               Rt + (size_t)pos0 * GW + s, rr, rz);
+      }
+      dftR<RL, true>(v);
+#pragma unroll
+      for (int e = 0; e < RL; ++e) buf[(blk * RL + e) * RS + s] = v[e];
+    }
+    __syncthreads();
+    FftRecButLast<N, N, true, GW>::run(buf, X0Addr{RS}, pl.tw, 1);
+    // ---- inverse group combine + store (registers) ----
+    for (int item = threadIdx.x; item < N * W; item += blockDim.x) {
+      const int w = item % W, x0 = item / W;
+      const size_t rbase = slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), 0) + c0 + w;
+      double2 v[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) v[g] = buf[x0 * RS + g * W + w];
+      reg_fft<G, true>(v, pl.tw, N);
+#pragma unroll
+      for (int g = 1; g < G; ++g) v[g] = cmulc(v[g], s_tw[g * W + w]);
+#pragma unroll
+      for (int g = 0; g < G; ++g) S[rbase + (size_t)g * sg.ncols] = v[g];
+    }
+    if (MODE != MID_APPLY) {
+      RState* st = ctl.st + b;
+      double t0, t1;
+      if (reduce2_last(rr, rz, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
+                       scratch, t0, t1)) {
+        const double inv = 1.0 / ((double)N * N * N);  // Parseval: (1/N^3) sum conj(X) Y
+        if (threadIdx.x == 0) mid_decide(st, ctl, b, it, t0 * inv, t1 * inv);
+      }
+    } else {
+      __syncthreads();
+    }
+  }
+}
+
 // Shared-memory stage kernel (any n; used for n >= 256).
 template <int N, int G, int W, int NB, int MODE>
 __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S, PlanDev pl,
@@ -877,44 +1028,6 @@ __global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S
 // ----------------------------------------------------------------------------
 // kernel 2b: register-resident spectral column pass (n <= 128)
 // ----------------------------------------------------------------------------
-// In-register in-place DIF / inverse DIT of length L on v[0..L): identical
-// index semantics to fft_smem<L> (digit-reversed output), all loops unrolled.
-template <int L, int M, bool INV>
-struct RegFft {
-  __device__ __forceinline__ static void run(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
-    constexpr int R = Radix<M>::value, S = M / R;
-    if constexpr (INV && S > 1) RegFft<L, S, true>::run(v, tw, ntab);
-#pragma unroll
-    for (int blk = 0; blk < L / M; ++blk) {
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        double2 a[R];
-#pragma unroll
-        for (int t = 0; t < R; ++t) a[t] = v[blk * M + j + t * S];
-        if constexpr (!INV) {
-          dftR<R, false>(a);
-          if (j > 0) {
-#pragma unroll
-            for (int m = 1; m < R; ++m) a[m] = cmul(a[m], __ldg(tw + (j * m) * (ntab / M)));
-          }
-        } else {
-          if (j > 0) {
-#pragma unroll
-            for (int m = 1; m < R; ++m) a[m] = cmulc(a[m], __ldg(tw + (j * m) * (ntab / M)));
-          }
-          dftR<R, true>(a);
-        }
-#pragma unroll
-        for (int t = 0; t < R; ++t) v[blk * M + j + t * S] = a[t];
-      }
-    }
-    if constexpr (!INV && S > 1) RegFft<L, S, false>::run(v, tw, ntab);
-  }
-};
-template <int L, bool INV>
-__device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
-  if constexpr (L > 1) RegFft<L, L, INV>::run(v, tw, ntab);
-}
 
 // Phase A (thread = column w, x0 offset j): the G-group combine and the first
 // radix-RA x0 stage straight from/to global memory in registers; phase B
