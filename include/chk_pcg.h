@@ -137,6 +137,22 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
                               void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * The same batched solve from HOST buffers (the reference-facing call: numpy
+ * in, numpy out).  beta_host [B][L^3], f_host [B][n^3] in, u_host [B][n^3]
+ * out; pinned host memory makes the copies asynchronous.  The batch runs in
+ * chunks of `chunk` realizations through two device slots: the upload of
+ * chunk c+1 and the download of chunk c-1 overlap the solve of chunk c.
+ * workspace: device buffer of chk_pcg_host_workspace_bytes bytes.
+ * ------------------------------------------------------------------------- */
+size_t chk_pcg_host_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, int32_t chunk,
+                                    int32_t max_iter);
+int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, const double* beta_host,
+                           const double* f_host, double* u_host, int32_t B, int32_t chunk,
+                           const chk_pcg_opts* opts, int32_t* iterations, double* final_rel,
+                           int32_t* status, int32_t* rhs_projected, double* history,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Slab decomposition of one grid over `nranks` GPUs (the
  * realization loop of ensemble_run, homogenize.py:133-182, shards instead).
  * Rank r owns planes x0 in [r n/P, (r+1) n/P) of p, u, f and one chunk of the

@@ -53,6 +53,9 @@ SIGNATURES = {
     "chk_pcg_workspace_bytes": (_sz, [_gp, _vp, _i32, _i32]),
     "chk_pcg_solve_batched": (_i32, [_gp, _vp, _vp, _vp, _vp, _i32, ctypes.POINTER(ChkPcgOpts),
                                      _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "chk_pcg_host_workspace_bytes": (_sz, [_gp, _vp, _i32, _i32]),
+    "chk_pcg_solve_host": (_i32, [_gp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.POINTER(ChkPcgOpts),
+                                  _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "chk_slab_exchange_elems": (_sz, [_gp, _vp, _i32]),
     "chk_slab_workspace_bytes": (_sz, [_gp, _vp, _vp, _i32, _i32]),
     "chk_slab_phase": (_i32, [_gp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

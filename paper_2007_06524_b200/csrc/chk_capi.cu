@@ -613,6 +613,102 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
   return CHK_OK;
 }
 
+size_t chk_pcg_host_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, int32_t chunk,
+                                    int32_t max_iter) {
+  if (!grid || !plan || chunk < 1 || max_iter < 1 || !supported_n(grid->n)) return 0;
+  const size_t nb = (size_t)grid->n * grid->n * grid->n;
+  const size_t lb = (size_t)grid->L * grid->L * grid->L;
+  const size_t slot = align_up(sizeof(double) * (2 * nb + lb) * chunk);
+  return 2 * slot + chk_pcg_workspace_bytes(grid, plan, chunk, max_iter);
+}
+
+int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, const double* beta_host,
+                           const double* f_host, double* u_host, int32_t B, int32_t chunk,
+                           const chk_pcg_opts* opts, int32_t* iterations, double* final_rel,
+                           int32_t* status, int32_t* rhs_projected, double* history,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (!grid || !plan || !beta_host || !f_host || !u_host || B < 1 || chunk < 1 || !opts)
+    return fail(CHK_EINVAL, "bad arguments");
+  if (chunk > B) chunk = B;
+  const size_t need = chk_pcg_host_workspace_bytes(grid, plan, chunk, opts->max_iter);
+  if (!workspace || workspace_bytes < need || need == 0) return fail(CHK_EINVAL, "workspace too small");
+  const size_t nb = (size_t)grid->n * grid->n * grid->n;
+  const size_t lb = (size_t)grid->L * grid->L * grid->L;
+  const size_t slot_bytes = align_up(sizeof(double) * (2 * nb + lb) * chunk);
+  char* base = static_cast<char*>(workspace);
+  double* d_f[2] = {reinterpret_cast<double*>(base), reinterpret_cast<double*>(base + slot_bytes)};
+  double* d_u[2] = {d_f[0] + nb * chunk, d_f[1] + nb * chunk};
+  double* d_b[2] = {d_u[0] + nb * chunk, d_u[1] + nb * chunk};
+  void* solver_ws = base + 2 * slot_bytes;
+  const size_t solver_bytes = workspace_bytes - 2 * slot_bytes;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t cp;
+  CHK_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+  cudaEvent_t in_ready[2], solved[2], out_done[2], start;
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&solved[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  int rc = CHK_OK;
+  long long launches = 0;
+  const int nchunks = (B + chunk - 1) / chunk;
+  auto upload = [&](int c) -> int {
+    const int b0 = c * chunk, nbc = (B - b0 < chunk) ? B - b0 : chunk, sl = c & 1;
+    CHK_CUDA(cudaMemcpyAsync(d_b[sl], beta_host + lb * b0, sizeof(double) * lb * nbc, cudaMemcpyHostToDevice, cp));
+    CHK_CUDA(cudaMemcpyAsync(d_f[sl], f_host + nb * b0, sizeof(double) * nb * nbc, cudaMemcpyHostToDevice, cp));
+    CHK_CUDA(cudaEventRecord(in_ready[sl], cp));
+    return CHK_OK;
+  };
+  CHK_CUDA(cudaEventRecord(start, s));  // the copies follow the caller's prior work
+  CHK_CUDA(cudaStreamWaitEvent(cp, start, 0));
+  if ((rc = upload(0))) goto done;
+  for (int c = 0; c < nchunks; ++c) {
+    const int b0 = c * chunk, nbc = (B - b0 < chunk) ? B - b0 : chunk, sl = c & 1;
+    if (c + 1 < nchunks && (rc = upload(c + 1))) goto done;  // overlaps the solve below
+    if (cudaStreamWaitEvent(s, in_ready[sl], 0) != cudaSuccess ||
+        (c >= 2 && cudaStreamWaitEvent(s, out_done[sl], 0) != cudaSuccess)) {
+      rc = fail(CHK_ECUDA, "stream wait failed");
+      goto done;
+    }
+    rc = chk_pcg_solve_batched(grid, plan, d_b[sl], d_f[sl], d_u[sl], nbc, opts, iterations ? iterations + b0 : nullptr,
+                               final_rel ? final_rel + b0 : nullptr, status ? status + b0 : nullptr,
+                               rhs_projected ? rhs_projected + b0 : nullptr,
+                               nullptr, solver_ws, solver_bytes, stream);
+    launches += g_launches;
+    if (rc) goto done;
+    if (history) {
+      // chk_pcg_solve_batched keeps the device history inside its workspace: copy it out
+      Workspace w = carve(solver_ws, grid->n, nbc, opts->max_iter);
+      if (cudaMemcpyAsync(history + (size_t)opts->max_iter * b0, w.hist, sizeof(double) * opts->max_iter * nbc,
+                          cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+        rc = fail(CHK_ECUDA, "history copy failed");
+        goto done;
+      }
+    }
+    if (cudaEventRecord(solved[sl], s) != cudaSuccess || cudaStreamWaitEvent(cp, solved[sl], 0) != cudaSuccess ||
+        cudaMemcpyAsync(u_host + nb * b0, d_u[sl], sizeof(double) * nb * nbc, cudaMemcpyDeviceToHost, cp) != cudaSuccess ||
+        cudaEventRecord(out_done[sl], cp) != cudaSuccess) {
+      rc = fail(CHK_ECUDA, "download failed");
+      goto done;
+    }
+  }
+  if (cudaStreamSynchronize(cp) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+    rc = fail(CHK_ECUDA, "final synchronize failed");
+done:
+  cudaStreamSynchronize(cp);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(in_ready[i]);
+    cudaEventDestroy(solved[i]);
+    cudaEventDestroy(out_done[i]);
+  }
+  cudaEventDestroy(start);
+  cudaStreamDestroy(cp);
+  g_launches = launches;
+  return rc;
+}
+
 }  // extern "C"
 
 // ----------------------------------------------------------------------------

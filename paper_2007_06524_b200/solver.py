@@ -193,6 +193,51 @@ def pcg_solve_batched(A, F, opts: SolveOptions | None = None, precond: Precondit
                        history=hist, launches=int(lib.chk_last_launch_count()))
 
 
+def pcg_solve_host(config, beta_host, F_host, opts: SolveOptions | None = None,
+                   precond: Preconditioner | None = None, chunk: int | None = None, out=None,
+                   record_history: bool = True, workspace: Workspace | None = None):
+    """Batched solve from HOST buffers (numpy / pinned torch CPU tensors): the
+    reference-facing call with host<->device copies inside.  The batch runs in
+    chunks with uploads/downloads overlapped with the solves (chk_pcg_solve_host).
+    Returns a BatchResult whose ``u`` is the host (B, n^3) array."""
+    torch = _lib.require_cuda()
+    opts = opts or SolveOptions()
+    n = config.n
+    if precond is None:
+        precond = make_preconditioner(3, n, opts)
+    plan = precond.plan
+    beta = beta_host if isinstance(beta_host, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(beta_host, dtype=np.float64)))
+    Fh = F_host if isinstance(F_host, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(F_host, dtype=np.float64)))
+    B = Fh.shape[0]
+    beta = beta.reshape(B, -1).contiguous()
+    Fh = Fh.reshape(B, -1).contiguous()
+    U = out if out is not None else torch.empty_like(Fh)
+    if chunk is None:
+        chunk = max(1, (B + 3) // 4)
+    grid = _lib.grid_struct(3, n, config.L, config.n0, config.k, config.offset, config.lam)
+    lib = _lib.load()
+    wb = int(lib.chk_pcg_host_workspace_bytes(ctypes.byref(grid), plan.handle, min(chunk, B), opts.max_iter))
+    if wb == 0:
+        raise ValueError("unsupported grid for the GPU path")
+    ws = (workspace or _default_ws).get(wb, torch.device("cuda", torch.cuda.current_device()))
+    its = np.zeros(B, np.int32)
+    fin = np.zeros(B)
+    st = np.zeros(B, np.int32)
+    proj = np.zeros(B, np.int32)
+    hist = np.zeros((B, opts.max_iter)) if record_history else None
+    copts = _lib.ChkPcgOpts(float(opts.tol), int(opts.max_iter), int(bool(opts.precond_residual_stopping)))
+    vp = ctypes.c_void_p
+    _lib.check(lib.chk_pcg_solve_host(
+        ctypes.byref(grid), plan.handle, vp(beta.data_ptr()), vp(Fh.data_ptr()), vp(U.data_ptr()), B,
+        int(chunk), ctypes.byref(copts), its.ctypes.data_as(vp), fin.ctypes.data_as(vp),
+        st.ctypes.data_as(vp), proj.ctypes.data_as(vp), hist.ctypes.data_as(vp) if hist is not None else None,
+        vp(ws.data_ptr()), ws.numel(), _lib.stream_handle()))
+    return BatchResult(u=U, iterations=its, final_residual=fin, status=st, rhs_projected=proj,
+                       history=hist, launches=int(lib.chk_last_launch_count()))
+
+
 def pcg_solve(A, f, opts: SolveOptions | None = None, precond: Preconditioner | None = None):
     """Drop-in for solver.py:118-194 on the GPU."""
     torch = _lib.require_cuda()

@@ -147,3 +147,20 @@ def test_acceptance_criterion_4_iteration_robustness():
             assert np.all(res.status == 0)
             worst[key] = max(worst[key], int(res.iterations.max()))
     assert worst["fourier"] <= 20 and worst["lkr"] <= 22, worst
+
+
+def test_host_buffer_pipeline_matches_device_batch():
+    """chk_pcg_solve_host (chunked, copies overlapped) = chk_pcg_solve_batched, bit for bit:
+    per-realization results do not depend on the batch composition."""
+    cfg = chk.LatticeConfig(d=3, L=8, n0=4, alpha="1/2", lam=0.1)
+    beta = np.stack([chk.sample_realization(cfg, chk.derive_seed(0, m)).beta_cells.ravel() for m in range(7)])
+    A = chk.StiffnessBatch(cfg, beta)
+    F = chk.corrector_rhs_batched(A, 1)
+    opts = chk.SolveOptions(tol=1e-8, preconditioner="lkr")
+    ref = chk.pcg_solve_batched(A, F, opts)
+    Fh = F.cpu().pin_memory()
+    res = chk.pcg_solve_host(cfg, torch.from_numpy(beta).pin_memory(), Fh, opts, chunk=3)
+    assert np.array_equal(res.iterations, ref.iterations)
+    assert np.array_equal(res.status, ref.status)
+    assert np.array_equal(res.history, ref.history)
+    assert torch.equal(res.u, ref.u.cpu())
