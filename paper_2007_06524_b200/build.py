@@ -11,12 +11,12 @@ REPO = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libchkpcg.so")
 SOURCES = [os.path.join(SRC, "chk_capi.cu")]
-DEPS = SOURCES + [os.path.join(SRC, f) for f in ("chk_fft.cuh", "chk_kernels.cuh")] + [
+DEPS = SOURCES + [os.path.join(SRC, f) for f in ("chk_fft.cuh", "chk_kernels.cuh", "chk_tma.cuh")] + [
     os.path.join(REPO, "include", "chk_pcg.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
+    "-O3", "-lineinfo", "-std=c++17", "-diag-suppress", "177",
     "-Xcompiler", "-fPIC", "-shared",
     "-I", os.path.join(REPO, "include"),
 ]

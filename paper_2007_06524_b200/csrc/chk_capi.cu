@@ -24,8 +24,8 @@ thread_local std::string g_err;
 thread_local long long g_launches = 0;
 
 // Optional per-kernel-class timing with CUDA events on the launching stream
-// (the bench's live roofline numbers).  Classes: 0 stencil_dot, 1 fwd_plane,
-// 2 mid_column, 3 inv_plane, 4 other.
+// (the bench's live roofline numbers).  Classes: 0 unused (was a separate
+// stencil kernel), 1 fwd_plane, 2 mid_column, 3 inv_plane, 4 other.
 struct Profiler {
   bool on = false;
   double ms[5] = {0, 0, 0, 0, 0};
@@ -122,6 +122,7 @@ struct Ops {
   static constexpr int TILES = NR * H / W;
   static constexpr int PLANE_BLOCKS = N * G;  // per realization
   static constexpr size_t plane_smem() { return (size_t)NR * H * sizeof(double2); }
+  // shared memory of the fused (n >= 256) middle kernel
   static size_t mid_smem(int r1) {
     return (size_t)mid_dsm_offset(N * (G * W + 1), G * W, r1) + (size_t)N * G * W * sizeof(double);
   }

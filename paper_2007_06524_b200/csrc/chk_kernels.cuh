@@ -1,23 +1,24 @@
 // chk_kernels.cuh -- sm_100a kernels of the batched PCG hot path.
 //
-// Per PCG iteration k >= 1 (pcg_solve loop, solver.py:161-185) four kernels run
-// over all B realizations of the batch (CTA = one (realization, x0-plane,
-// x1-group) slab or one spectral column tile):
+// One PCG iteration k >= 1 (pcg_solve loop, solver.py:161-185) is three
+// kernels over all B realizations of the batch:
 //
-//   stencil_dot   pq  = <p, A p>                                  (solver.py:162-165)
-//   fwd_plane     u += a p ; r -= a A p ; ||r||^2 ; stop test ;    (solver.py:166-177)
-//                 then R2C along x2 + C2C along the x1 group of r
-//   mid_column    C2C along x1 (group combine) and x0, scale by the  (lowrank.py:189-192)
-//                 rank-R canonical diagonal evaluated on the fly,
-//                 <r, z> by Parseval, inverse along x0 / x1 group
-//   inv_plane     inverse C2C x1 group + C2R x2 -> z ; p = z + b p  (solver.py:179-185)
+//   fwd_plane<FWD_Q>   q = A p (matrix-free 7-point stencil from the L^3 cell
+//                      array), <p, q> -> alpha; R2C along x2 and C2C along the
+//                      x1 group of q in shared memory        (solver.py:162-166)
+//   mid_column*        group combine + x0 transform of Q, R -= alpha Q (the
+//                      residual is kept as its spectrum), ||r||^2 (stop test),
+//                      z = D R with D[i,j,l] = sum_k U0[k,i]U1[k,j]U2[k,l]
+//                      evaluated per column tile (never materialised), r.z,
+//                      inverse x0 / group combine            (solver.py:168-183)
+//   inv_plane<INV_ITER> inverse x1-group C2C + C2R -> z; u += alpha p;
+//                      p = z + beta p                         (solver.py:167,184)
 //
-// The stiffness never exists as a matrix: A is the 7-point edge-weighted
-// stencil of tests/oracles.py:35-82 with edge conductivities built from the
-// compact L^3 cell array on the fly.  The diagonal D[i,j,l] = sum_k U0[k,i]
-// U1[k,j] U2[k,l] is never materialised.  Reductions are deterministic: every
-// CTA writes a partial, the last CTA of the realization (atomic ticket) sums
-// them in a fixed order and takes the scalar decisions (alpha, beta, stop).
+// CTA = one (realization, x0-plane, x1-group) slab or one spectral column tile.
+// Reductions are deterministic: every CTA writes a partial, the last CTA of the
+// realization (atomic ticket) sums them in a fixed order and takes the scalar
+// decisions (alpha, breakdown, stop, beta) -- or, when one grid is
+// slab-decomposed over GPUs, publishes rank-local sums for an allreduce.
 #pragma once
 #include "chk_fft.cuh"
 #include "chk_tma.cuh"
@@ -926,90 +927,6 @@ __global__ void __launch_bounds__(256) mid_column_fused_kernel(double2* __restri
       for (int g = 1; g < G; ++g) v[g] = cmulc(v[g], s_tw[g * W + w]);
 #pragma unroll
       for (int g = 0; g < G; ++g) S[rbase + (size_t)g * sg.ncols] = v[g];
-    }
-    if (MODE != MID_APPLY) {
-      RState* st = ctl.st + b;
-      double t0, t1;
-      if (reduce2_last(rr, rz, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
-                       scratch, t0, t1)) {
-        const double inv = 1.0 / ((double)N * N * N);  // Parseval: (1/N^3) sum conj(X) Y
-        if (threadIdx.x == 0) mid_decide(st, ctl, b, it, t0 * inv, t1 * inv);
-      }
-    } else {
-      __syncthreads();
-    }
-  }
-}
-
-// Shared-memory stage kernel (any n; used for n >= 256).
-template <int N, int G, int W, int NB, int MODE>
-__global__ void __launch_bounds__(256) mid_column_kernel(double2* __restrict__ S, PlanDev pl,
-                                                         SolveCtl ctl, SlabGeo sg, int it, int B) {
-  constexpr int NR = N / G;
-  constexpr int N2 = N / 2;
-  constexpr int H = N2 + 1;
-  const int TILES = sg.tiles;  // tiles of this rank (all NR*H/W when not slab-decomposed)
-  const int nsh = __ffs(sg.nloc) - 1;  // nloc is a power of two
-  constexpr int GW = G * W;
-  constexpr int RS = GW + 1;
-  extern __shared__ double2 buf[];  // [N][RS] data tile (aliased by the [r1][GW] coefficients)
-  const int doff = mid_dsm_offset(N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
-  double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
-  __shared__ double scratch[32];
-  __shared__ int s_k1[GW], s_k2[GW];
-  __shared__ double s_wgt[GW];
-  __shared__ double2 s_tw[GW];
-  __shared__ int s_act[NB];
-  __shared__ double s_alpha[NB];
-  const int bg = blockIdx.x / TILES;
-  const int tile = blockIdx.x - bg * TILES;
-  const int c0 = tile * W;                       // first column inside this rank's chunk
-  const int cg0 = (sg.tile_off + tile) * W;      // global spectral column
-  const int b0 = bg * NB;
-  if (threadIdx.x == 0) {
-    int any = 0;
-    for (int j = 0; j < NB; ++j) {
-      const int b = b0 + j;
-      int a = (b < B);
-      if (a && MODE != MID_APPLY) a = (ctl.st[b].status == ST_ACTIVE);
-      s_act[j] = a;
-      s_alpha[j] = (a && MODE == MID_ITER) ? ctl.st[b].alpha : 0.0;
-      any |= a;
-    }
-    scratch[0] = any;
-  }
-  __syncthreads();
-  if (scratch[0] == 0.0) return;
-  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
-
-  const double scale = 2.0 / ((double)N * N * N);
-  for (int j = 0; j < NB; ++j) {
-    if (!s_act[j]) continue;
-    const int b = b0 + j;
-    for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
-      const int w = i % W, gq = (i / W) % G, x0 = i / GW;
-      double2 v = S[slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), gq) + c0 + w];
-      if (G > 1) v = cmul(v, s_tw[gq * W + w]);
-      buf[x0 * RS + gq * W + w] = v;
-    }
-    __syncthreads();
-    if (G > 1) fft_smem<G, false, N * W>(buf, GAddr<W>{RS}, pl.tw, N);
-    fft_smem<N, false, GW>(buf, X0Addr{RS}, pl.tw, N);
-    double rr = 0.0, rz = 0.0;
-    double2* Rt = ctl.Rh + ((size_t)b * TILES + tile) * N * GW;
-    for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
-      const int s = i % GW, pos0 = i / GW;
-      buf[pos0 * RS + s] = mid_point<MODE>(buf[pos0 * RS + s], Dsm[pos0 * GW + s], s_wgt[s], scale,
-                                           s_alpha[j], Rt + i, rr, rz);
-    }
-    __syncthreads();
-    fft_smem<N, true, GW>(buf, X0Addr{RS}, pl.tw, N);
-    if (G > 1) fft_smem<G, true, N * W>(buf, GAddr<W>{RS}, pl.tw, N);
-    for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
-      const int w = i % W, gq = (i / W) % G, x0 = i / GW;
-      double2 v = buf[x0 * RS + gq * W + w];
-      if (G > 1) v = cmulc(v, s_tw[gq * W + w]);
-      S[slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), gq) + c0 + w] = v;
     }
     if (MODE != MID_APPLY) {
       RState* st = ctl.st + b;
