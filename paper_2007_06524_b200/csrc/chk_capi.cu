@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/chk_pcg.h"
@@ -109,7 +110,7 @@ template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16, NB = 4, REG =
 template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 16, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<128> { static constexpr int G = 2,  W = CHK_W128, NB = 16, REG = 1, RA = 8, P = 1; };
-template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 4, REG = 0, RA = 1, P = 1; };
+template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 16, REG = 0, RA = 1, P = 1; };
 template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2, REG = 0, RA = 1, P = 1; };
 
 // every h-cell inside its sub-cell (alpha = 1/2): stencil fast path
@@ -183,15 +184,22 @@ struct Ops {
   static int mid(int mode, cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it,
                  SlabGeo sg = whole()) {
     ProfScope ps(2, s);
-    // amortise the diagonal over NB realizations when that still fills the GPU
-    const bool wide = ((B + NB - 1) / NB) * sg.tiles >= 2 * 148;
+    // amortise the diagonal over NB realizations per CTA when that still gives
+    // >= 2 CTAs per SM (measured: the diagonal tile costs more than wave fill)
+    const int pick = ((long long)((B + NB - 1) / NB) * sg.tiles >= 2LL * 148) ? NB : 1;
     int rc;
+    auto go = [&](auto mode_tag) -> int {
+      constexpr int M = decltype(mode_tag)::value;
+      if (pick == NB) return mid_launch<NB, M>(s, B, S, pl, ctl, it, sg);
+      if (pick == 4) return mid_launch<(NB > 4 ? 4 : NB), M>(s, B, S, pl, ctl, it, sg);
+      return mid_launch<1, M>(s, B, S, pl, ctl, it, sg);
+    };
     if (mode == MID_APPLY)
-      rc = wide ? mid_launch<NB, MID_APPLY>(s, B, S, pl, ctl, it, sg) : mid_launch<1, MID_APPLY>(s, B, S, pl, ctl, it, sg);
+      rc = go(std::integral_constant<int, MID_APPLY>{});
     else if (mode == MID_INIT)
-      rc = wide ? mid_launch<NB, MID_INIT>(s, B, S, pl, ctl, it, sg) : mid_launch<1, MID_INIT>(s, B, S, pl, ctl, it, sg);
+      rc = go(std::integral_constant<int, MID_INIT>{});
     else
-      rc = wide ? mid_launch<NB, MID_ITER>(s, B, S, pl, ctl, it, sg) : mid_launch<1, MID_ITER>(s, B, S, pl, ctl, it, sg);
+      rc = go(std::integral_constant<int, MID_ITER>{});
     if (rc) return rc;
     CHK_LAUNCHED();
     return CHK_OK;
