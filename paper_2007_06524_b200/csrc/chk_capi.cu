@@ -101,7 +101,7 @@ template <int N>
 struct Cfg;
 // NB realizations share one evaluation of the diagonal tile in the middle pass.
 #ifndef CHK_W128
-#define CHK_W128 16
+#define CHK_W128 8
 #endif
 // REG: register-resident middle pass (first x0 radix RA in phase A, P
 // realizations in flight per CTA); otherwise the shared-memory stage kernel.
@@ -120,6 +120,10 @@ template <int N>
 struct Ops {
   static constexpr int G = Cfg<N>::G, W = Cfg<N>::W, NB = Cfg<N>::NB, NR = N / G, H = N / 2 + 1;
   static constexpr int REG = Cfg<N>::REG, RA = Cfg<N>::RA, P = Cfg<N>::P;
+#ifndef CHK_STAGE
+#define CHK_STAGE 1
+#endif
+  static constexpr bool STG = CHK_STAGE && (N == 64 || N == 128);
   static constexpr int TILES = NR * H / W;
   static constexpr int PLANE_BLOCKS = N * G;  // per realization
   static constexpr size_t plane_smem() { return (size_t)NR * H * sizeof(double2); }
@@ -171,9 +175,11 @@ struct Ops {
     if constexpr (REG) {
       constexpr int PX = (NBX == 1) ? 1 : P;
       constexpr int NT = (W * (N / RA) > 128 ? 256 : 128) * PX;
-      const size_t sm = (size_t)mid_dsm_offset(PX * N * (G * W + 1), G * W, r1) + (size_t)N * G * W * sizeof(double);
-      CHK_CUDA(allow_smem(mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT>, sm));
-      mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT><<<grid, NT, sm, s>>>(S, pl, ctl, sg, it, B);
+      constexpr bool SX = STG && PX == 1 && W * (N / RA) == NT;
+      size_t sm = (size_t)mid_dsm_offset(PX * N * (G * W + 1), G * W, r1) + (((size_t)N * G * W * sizeof(double) + 15) & ~(size_t)15);
+      if (SX) sm += (size_t)G * RA * NT * sizeof(double2);
+      CHK_CUDA(allow_smem(mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT, SX>, sm));
+      mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT, SX><<<grid, NT, sm, s>>>(S, pl, ctl, sg, it, B);
     } else {
       const size_t sm = mid_smem(r1);
       CHK_CUDA(allow_smem(mid_column_fused_kernel<N, G, W, NBX, MODE>, sm));

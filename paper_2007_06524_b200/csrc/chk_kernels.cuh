@@ -952,8 +952,14 @@ __global__ void __launch_bounds__(256) mid_column_fused_kernel(double2* __restri
 // residual update / diagonal scaling and the inverse stages in registers.
 // Shared memory is touched twice per element per direction (one exchange each
 // way).  P realizations are in flight per CTA; NB share one diagonal tile.
-template <int N, int G, int W, int RA, int NB, int P, int MODE, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* __restrict__ S, PlanDev pl,
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int N, int G, int W, int RA, int NB, int P, int MODE, int NT, bool STG = false>
+__global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kernel(double2* __restrict__ S, PlanDev pl,
                                                                       SolveCtl ctl, SlabGeo sg, int it, int B) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
@@ -997,13 +1003,32 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
   }
   __syncthreads();
   if (scratch[0] == 0.0) return;
+  // STG: the phase-A tile of the next realization streams into a per-thread
+  // staging area (cp.async) while the current one is transformed
+  static_assert(!STG || (P == 1 && ITEMS_A == NT), "staging needs one phase-A item per thread");
+  double2* stg = reinterpret_cast<double2*>(reinterpret_cast<char*>(Dsm) + ((N * GW * 8 + 15) & ~15));
+  auto stage = [&](int cc) {
+    if constexpr (STG) {
+      if (sg.P == 1 && s_act[cc]) {
+        const int w = threadIdx.x % W, j = threadIdx.x / W;
+        const double2* base = S + ((size_t)(b0 + cc) * N + j) * G * (size_t)sg.ncols + c0 + w;
+#pragma unroll
+        for (int t = 0; t < RA; ++t)
+#pragma unroll
+          for (int g = 0; g < G; ++g)
+            cp_async16(stg + (g * RA + t) * NT + threadIdx.x, base + (size_t)(JA * t * G + g) * sg.ncols);
+      }
+      cp_async_commit();
+    }
+  };
+  stage(0);
   mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
 
   const double scale = 2.0 / ((double)N * N * N);
   const int ntab = N;
   for (int c = 0; c < NB / P; ++c) {
     // warm L2 with the next chunk's tile rows (W * 16 B per (x0, group) row)
-    if (c + 1 < NB / P) {
+    if (!STG && c + 1 < NB / P) {
       for (int i = threadIdx.x; i < P * N * G; i += blockDim.x) {
         const int pr = i / (N * G), rr = i - pr * (N * G);
         if (s_act[(c + 1) * P + pr])
@@ -1019,7 +1044,13 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
       const int w = ia % W, j = ia / W;
       const int bb = b0 + c * P + pr;
       double2 v[G][RA];
-      if (sg.P == 1) {  // single chunk: rows are linear in x0
+      if (STG && sg.P == 1) {
+        cp_async_wait_all();
+#pragma unroll
+        for (int t = 0; t < RA; ++t)
+#pragma unroll
+          for (int g = 0; g < G; ++g) v[g][t] = stg[(g * RA + t) * NT + threadIdx.x];
+      } else if (sg.P == 1) {  // single chunk: rows are linear in x0
         const double2* base = S + ((size_t)bb * N + j) * G * (size_t)sg.ncols + c0 + w;
 #pragma unroll
         for (int t = 0; t < RA; ++t)
@@ -1074,6 +1105,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) mid_column_reg_kernel(double2* _
       }
     }
     __syncthreads();
+    if (c + 1 < NB / P) stage(c + 1);  // overlaps phases B and A-inverse
     // ---- phase B: remaining stages, residual update / diagonal, inverse ----
     double accr[P], accz[P];
 #pragma unroll

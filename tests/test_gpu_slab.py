@@ -44,7 +44,7 @@ def _slab(cfg, beta, F, opts, P):
     return res, u
 
 
-@pytest.mark.parametrize("cfg_id,ms,P", [(2, [0, 1, 2], 2), (2, [3], 4), (3, [0, 1], 4), (4, [0], 2)])
+@pytest.mark.parametrize("cfg_id,ms,P", [(2, [0, 1, 2], 2), (2, [3], 4), (3, [0, 1], 8), (4, [0], 2)])
 def test_slab_matches_single_gpu(cfg_id, ms, P):
     cfg, beta, A, F, opts = _problem(cfg_id, ms)
     ref = chk.pcg_solve_batched(A, F, opts)
