@@ -21,6 +21,7 @@ compiled or shipped), process pool over all host threads, bounded sample.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -210,13 +211,10 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     ms = float(ev0.elapsed_time(ev1))
-    prof_ms = (ctypes_array := np.zeros(5, dtype=np.float64))
+    prof_ms = np.zeros(5, dtype=np.float64)
     prof_n = np.zeros(5, dtype=np.int64)
-    import ctypes
-
     lib.chk_profile_read(prof_ms.ctypes.data_as(ctypes.c_void_p), prof_n.ctypes.data_as(ctypes.c_void_p))
     lib.chk_profile_enable(0)
-    del ctypes_array
 
     # --- e2e: reference-facing call with host buffers --------------------------
     # chk_pcg_solve_host: pinned numpy-side inputs/outputs, the batch streamed
