@@ -232,7 +232,8 @@ def run_ours(args):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        res_e = chk.pcg_solve_host(lat, beta_h, F_h, opts, P, out=U_h, record_history=False, workspace=ws_h)
+        res_e = chk.pcg_solve_host(lat, beta_h, F_h, opts, P, out=U_h, record_history=False, workspace=ws_h,
+                                   chunk=args.e2e_chunk or None)
         t1.record(stream)
         barrier()
         if step >= args.warmup:
@@ -498,6 +499,8 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=sorted(CFG))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=0,
+                    help="realizations per pipelined chunk of the host-buffer solve (default B/4)")
     ap.add_argument("--slab", action="store_true",
                     help="force the slab-decomposed path (default for config 5 when N > 1)")
     args = ap.parse_args()

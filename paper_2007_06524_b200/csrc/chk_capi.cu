@@ -140,11 +140,17 @@ struct Ops {
   }
   static bool slab_ok(int P) { return P >= 1 && N % P == 0 && (N / P) >= 1 && TILES % P == 0 && P <= 64; }
 
+  // raise the dynamic shared-memory limit once per kernel instantiation and size
   template <class K>
   static cudaError_t allow_smem(K kernel, size_t bytes) {
-    if (bytes > 48 * 1024)
-      return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    return cudaSuccess;
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    static thread_local std::vector<std::pair<const void*, size_t>> done;
+    const void* key = reinterpret_cast<const void*>(kernel);
+    for (auto& d : done)
+      if (d.first == key && d.second >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.push_back({key, bytes});
+    return e;
   }
 
   static int fwd(int mode, cudaStream_t s, int B, Geo g, const double* beta, const double* src,
