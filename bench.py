@@ -64,7 +64,7 @@ def kernel_bytes_per_dof(n):
     }
 
 
-KERNEL_CLASSES = ["stencil_dot", "fwd_plane", "mid_column", "inv_plane"]  # index = profiler class
+KERNEL_CLASSES = ["stencil_dot", "fwd_plane", "mid_column", "inv_plane", "plane_pair"]  # index = profiler class
 B_ALG = 104.0  # SURVEY §8d algorithmic bytes per DOF-iteration (whole iteration)
 
 
@@ -263,6 +263,16 @@ def run_ours(args):
         per_kernel = {}
         kb = kernel_bytes_per_dof(n)
         dof_it_rank = dof_its  # rank 0's own work, for the live kernel figures
+        if prof_n[4] > 0:
+            # paired solve: every realization-iteration runs one forward and one inverse
+            # plane pass, nearly all of them inside pair_plane launches (the first forward
+            # and the last inverse pass of a half run alone): account the three classes
+            # together as one kernel doing fwd + inv bytes per DOF-iteration
+            kb["plane_pair"] = kb["fwd_plane"] + kb["inv_plane"]
+            prof_ms[4] += prof_ms[1] + prof_ms[3]
+            prof_n[4] += prof_n[1] + prof_n[3]
+            prof_ms[1] = prof_ms[3] = 0.0
+            prof_n[1] = prof_n[3] = 0
         for i, name in enumerate(KERNEL_CLASSES):
             if name not in kb or prof_n[i] == 0 or prof_ms[i] <= 0:
                 continue
@@ -272,7 +282,7 @@ def run_ours(args):
                                 "alg_bytes_per_dof": round(kb[name], 3),
                                 "achieved_gbs": round(achieved, 1),
                                 "frac": round(achieved / peak, 3),
-                                "share": round(prof_ms[i] / max(1e-9, prof_ms[:4].sum()), 3)}
+                                "share": round(prof_ms[i] / max(1e-9, prof_ms.sum()), 3)}
         dom = max(per_kernel, key=lambda k: per_kernel[k]["ms_total"]) if per_kernel else None
         traffic = None
         prof_json = os.path.join(REPO, "profiles", "ncu_traffic.json")
@@ -280,7 +290,7 @@ def run_ours(args):
             # ncu --set full dram__bytes_read+write of the same kernel (profiles/), per DOF,
             # scaled to the DOF one launch processes on average in this run
             ncu_name = {"fwd_plane": "fwd_plane_kernel", "mid_column": "mid_column_reg_kernel",
-                        "inv_plane": "inv_plane_kernel"}.get(dom)
+                        "inv_plane": "inv_plane_kernel", "plane_pair": "pair_plane_kernel"}.get(dom)
             tj = json.load(open(prof_json)).get(f"config{cfg_id}", {}).get(ncu_name)
             if tj:
                 per_launch_dof = dof_it_rank / max(1, per_kernel[dom]["launches"])

@@ -234,6 +234,22 @@ struct Ops {
     CHK_LAUNCHED();
     return CHK_OK;
   }
+  // paired plane pass (pair_plane_kernel): fa.blocks forward + ia.blocks inverse CTAs
+  static int pair(cudaStream_t s, const FwdArgs& fa, const InvArgs& ia, PlanDev pl) {
+    const size_t sm = plane_smem();
+    const SlabGeo sg = whole();
+    dim3 grid(fa.blocks + ia.blocks), block(256);
+    ProfScope ps(4, s);
+    if (allin(fa.g)) {
+      CHK_CUDA(allow_smem(pair_plane_kernel<N, G, true>, sm));
+      pair_plane_kernel<N, G, true><<<grid, block, sm, s>>>(fa, ia, pl, sg);
+    } else {
+      CHK_CUDA(allow_smem(pair_plane_kernel<N, G, false>, sm));
+      pair_plane_kernel<N, G, false><<<grid, block, sm, s>>>(fa, ia, pl, sg);
+    }
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
   static int stencil(cudaStream_t s, int B, Geo g, const double* beta, const double* x, double* y,
                      double* xy, double* part, unsigned* cnt) {
     if (allin(g))
@@ -272,6 +288,23 @@ struct Ops {
     case 512: { using O = Ops<512>; __VA_ARGS__; } break;  \
     default: return fail(CHK_EUNSUPPORTED, "unsupported n " + std::to_string(n)); \
   }
+
+// Realizations in the first half of a paired solve (0: unpaired).  Pairing pays
+// only while each half alone still runs the middle pass with the diagonal tile
+// amortised over NB realizations on >= 2 CTAs per SM (measured: config 3 +3 %,
+// config 2 -25 % when its 32-realization halves lose the NB grouping, config 4
+// neutral).  CHK_PAIR=0 disables it, CHK_PAIR=2 forces it for any B >= 2 (tests).
+template <class O>
+int pair_split(int B) {
+  const char* e = getenv("CHK_PAIR");
+  const int env = e ? atoi(e) : 1;
+  if (env == 2 && B >= 2) return B / 2;
+  if (!env || !O::REG || B < 2 * O::NB) return 0;
+  const int Ba = (B / 2) / O::NB * O::NB;
+  const int Bb = B - Ba;
+  const long long ctas = (long long)(Ba / O::NB) * O::TILES;
+  return (ctas >= 2LL * 148 && Bb >= Ba) ? Ba : 0;
+}
 
 bool supported_n(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
 
@@ -582,20 +615,19 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
       const int chunk = (n >= 128) ? 2 : 8;
       bool pending = false;
       int ev_i = 0;
-      for (int it = 1; it <= opts->max_iter; ++it) {
-        // q = A p, p.q, alpha; Q = FFT(q)            (solver.py:162-166)
-        if ((rc2 = O::fwd(FWD_Q, s, B, g, beta, w.p, u, w.S, pl, ctl, it))) return rc2;
-        // R -= alpha Q, stop test, z = P r, r.z, beta (solver.py:168-183)
-        if ((rc2 = O::mid(MID_ITER, s, B, w.S, pl, ctl, it))) return rc2;
-        // u += alpha p, p = z + beta p                (solver.py:167,184)
-        if ((rc2 = O::inv(INV_ITER, s, B, w.S, w.p, u, pl, ctl, it))) return rc2;
+      // poll: true when the previous chunk's status copy shows no active realization
+      auto poll = [&](int it, bool& stop) -> int {
+        stop = false;
         if (it % chunk == 0 || it == opts->max_iter) {
           if (pending) {
             CHK_CUDA(cudaEventSynchronize(ev[ev_i ^ 1]));
             const RState* prev = hst_all + (size_t)(ev_i ^ 1) * B;
             bool any = false;
             for (int b = 0; b < B; ++b) any |= (prev[b].status == ST_ACTIVE);
-            if (!any) break;
+            if (!any) {
+              stop = true;
+              return CHK_OK;
+            }
           }
           CHK_CUDA(cudaMemcpyAsync(hst_all + (size_t)ev_i * B, w.st, sizeof(RState) * B,
                                    cudaMemcpyDeviceToHost, s));
@@ -603,6 +635,61 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
           ev_i ^= 1;
           pending = true;
         }
+        return CHK_OK;
+      };
+      const int Ba = pair_split<O>(B);
+      if (Ba > 0) {
+        // Two halves half an iteration apart; every plane launch pairs the forward
+        // pass of one half with the inverse pass of the other (pair_plane_kernel):
+        //   fwd(A,1) mid(A,1) | [inv(A,k) fwd(B,k)] mid(B,k) [fwd(A,k+1) inv(B,k)] mid(A,k+1) | ...
+        const size_t nb = (size_t)n * n * n, spec = (size_t)n * n * (n / 2 + 1);
+        const size_t lb = (size_t)g.L * g.L * g.L;
+        auto fargs = [&](int b0, int Bn, int it) {
+          SolveCtl c = ctl;
+          c.st += b0; c.Rh += spec * b0; c.part += (size_t)2 * ctl.maxblk * b0; c.hist += (size_t)ctl.max_iter * b0;
+          return FwdArgs{g, beta + lb * b0, w.p + nb * b0, u + nb * b0, w.S + spec * b0, c, Bn, it, Bn * O::PLANE_BLOCKS};
+        };
+        auto iargs = [&](int b0, int Bn, int it) {
+          const FwdArgs f = fargs(b0, Bn, it);
+          return InvArgs{f.S, w.p + nb * b0, f.u, f.ctl, Bn, it, Bn * O::PLANE_BLOCKS};
+        };
+        const int Bb = B - Ba;
+        const FwdArgs A1 = fargs(0, Ba, 1);
+        if ((rc2 = O::fwd(FWD_Q, s, Ba, g, A1.beta, A1.p, A1.u, A1.S, pl, A1.ctl, 1))) return rc2;
+        if ((rc2 = O::mid(MID_ITER, s, Ba, A1.S, pl, A1.ctl, 1))) return rc2;
+        int a_pending = 1;  // iteration of half A whose inverse pass is still to run
+        for (int it = 1; it <= opts->max_iter; ++it) {
+          const FwdArgs Bf = fargs(Ba, Bb, it);
+          if ((rc2 = O::pair(s, Bf, iargs(0, Ba, it), pl))) return rc2;
+          a_pending = 0;
+          if ((rc2 = O::mid(MID_ITER, s, Bb, Bf.S, pl, Bf.ctl, it))) return rc2;
+          if (it < opts->max_iter) {
+            if ((rc2 = O::pair(s, fargs(0, Ba, it + 1), iargs(Ba, Bb, it), pl))) return rc2;
+            if ((rc2 = O::mid(MID_ITER, s, Ba, A1.S, pl, fargs(0, Ba, it + 1).ctl, it + 1))) return rc2;
+            a_pending = it + 1;
+          } else {
+            const InvArgs Bi = iargs(Ba, Bb, it);
+            if ((rc2 = O::inv(INV_ITER, s, Bb, Bi.S, Bi.p, Bi.u, pl, Bi.ctl, it))) return rc2;
+          }
+          bool stop;
+          if ((rc2 = poll(it, stop))) return rc2;
+          if (stop) break;
+        }
+        if (a_pending) {  // half A's last middle pass ran: finish its u update
+          const InvArgs Ai = iargs(0, Ba, a_pending);
+          if ((rc2 = O::inv(INV_ITER, s, Ba, Ai.S, Ai.p, Ai.u, pl, Ai.ctl, a_pending))) return rc2;
+        }
+      } else
+      for (int it = 1; it <= opts->max_iter; ++it) {
+        // q = A p, p.q, alpha; Q = FFT(q)            (solver.py:162-166)
+        if ((rc2 = O::fwd(FWD_Q, s, B, g, beta, w.p, u, w.S, pl, ctl, it))) return rc2;
+        // R -= alpha Q, stop test, z = P r, r.z, beta (solver.py:168-183)
+        if ((rc2 = O::mid(MID_ITER, s, B, w.S, pl, ctl, it))) return rc2;
+        // u += alpha p, p = z + beta p                (solver.py:167,184)
+        if ((rc2 = O::inv(INV_ITER, s, B, w.S, w.p, u, pl, ctl, it))) return rc2;
+        bool stop;
+        if ((rc2 = poll(it, stop))) return rc2;
+        if (stop) break;
       }
       if ((rc2 = O::mean_u(s, B, u, ctl))) return rc2;
     });

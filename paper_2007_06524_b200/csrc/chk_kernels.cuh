@@ -534,12 +534,13 @@ __device__ __forceinline__ void ld4v(const double* p, double (&v)[4]) {
                : "l"(p));
 }
 
+// CTA body, `bid` = plane block index (blockIdx.x of the stand-alone kernel)
 template <int N, int G, int MODE, bool ALLIN>
-__global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __restrict__ beta,
-                                                        const double* __restrict__ src,  // x (APPLY) / f (INIT) / p (Q)
-                                                        double* __restrict__ u,
-                                                        double2* __restrict__ S, PlanDev pl,
-                                                        SolveCtl ctl, SlabGeo sg, int B, int it) {
+__device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __restrict__ beta,
+                                               const double* __restrict__ src,  // x (APPLY) / f (INIT) / p (Q)
+                                               double* __restrict__ u, double2* __restrict__ S,
+                                               const PlanDev& pl, const SolveCtl& ctl, const SlabGeo& sg,
+                                               int B, int it, int bid) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
@@ -547,8 +548,8 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
   extern __shared__ double2 buf[];
   __shared__ double scratch[32];
   const int nlg = sg.nloc * G;
-  const int b = blockIdx.x / nlg;
-  const int rem = blockIdx.x - b * nlg;
+  const int b = bid / nlg;
+  const int rem = bid - b * nlg;
   const int x0l = rem / G, gg = rem - (rem / G) * G;  // local plane, x1 group
   const int x0 = sg.x0_off + x0l;                     // global plane
   const size_t nn = (size_t)N * N;
@@ -626,6 +627,14 @@ __global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __r
     bulk_commit();
     bulk_wait_read0();
   }
+}
+
+template <int N, int G, int MODE, bool ALLIN>
+__global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __restrict__ beta,
+                                                        const double* __restrict__ src, double* __restrict__ u,
+                                                        double2* __restrict__ S, PlanDev pl,
+                                                        SolveCtl ctl, SlabGeo sg, int B, int it) {
+  fwd_plane_body<N, G, MODE, ALLIN>(g, beta, src, u, S, pl, ctl, sg, B, it, blockIdx.x);
 }
 
 // ----------------------------------------------------------------------------
@@ -1228,9 +1237,9 @@ __device__ __forceinline__ void stv4(double* p, const double (&v)[4]) {
 }
 
 template <int N, int G, int MODE>
-__global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restrict__ S,
-                                                        double* __restrict__ out, double* __restrict__ u,
-                                                        PlanDev pl, SolveCtl ctl, SlabGeo sg, int B, int it) {
+__device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, double* __restrict__ out,
+                                               double* __restrict__ u, const PlanDev& pl, const SolveCtl& ctl,
+                                               const SlabGeo& sg, int B, int it, int bid) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
@@ -1238,8 +1247,8 @@ __global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restric
   extern __shared__ double2 buf[];
   __shared__ alignas(8) uint64_t bar;
   const int nlg = sg.nloc * G;
-  const int b = blockIdx.x / nlg;
-  const int rem = blockIdx.x - b * nlg;
+  const int b = bid / nlg;
+  const int rem = bid - b * nlg;
   const int x0 = rem / G, gg = rem - (rem / G) * G;  // local plane, x1 group
   const size_t nb = (size_t)sg.nloc * N * N;
   double alpha = 0.0, beta = 0.0;
@@ -1309,6 +1318,54 @@ __global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restric
       }
     }
   }
+}
+
+template <int N, int G, int MODE>
+__global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restrict__ S,
+                                                        double* __restrict__ out, double* __restrict__ u,
+                                                        PlanDev pl, SolveCtl ctl, SlabGeo sg, int B, int it) {
+  inv_plane_body<N, G, MODE>(S, out, u, pl, ctl, sg, B, it, blockIdx.x);
+}
+
+// Paired plane pass: the forward pass of one half of the batch (q = A p, FFT;
+// fp64-pipe and latency heavy) and the inverse pass of the other half (iFFT,
+// u / p updates; HBM heavy) in ONE launch, their CTAs interleaved so that both
+// kinds are co-resident on every SM.  The two halves are half an iteration
+// apart (solver driver), so the launch has no internal dependency.
+struct FwdArgs {
+  Geo g;
+  const double* beta;
+  const double* p;
+  double* u;
+  double2* S;
+  SolveCtl ctl;
+  int B, it, blocks;
+};
+struct InvArgs {
+  const double2* S;
+  double* p;
+  double* u;
+  SolveCtl ctl;
+  int B, it, blocks;
+};
+
+template <int N, int G, bool ALLIN>
+__global__ void __launch_bounds__(256, 3) pair_plane_kernel(FwdArgs fa, InvArgs ia, PlanDev pl, SlabGeo sg) {
+  const int m = fa.blocks < ia.blocks ? fa.blocks : ia.blocks;
+  const int bx = blockIdx.x;
+  bool fwd;
+  int bid;
+  if (bx < 2 * m) {
+    fwd = (bx & 1) == 0;
+    bid = bx >> 1;
+  } else {
+    fwd = fa.blocks > m;
+    bid = bx - m;
+  }
+  if (fwd)
+    fwd_plane_body<N, G, FWD_Q, ALLIN>(fa.g, fa.beta, fa.p, fa.u, fa.S, pl, fa.ctl, sg, fa.B, fa.it, bid);
+  else
+    inv_plane_body<N, G, INV_ITER>(ia.S, ia.p, ia.u, pl, ia.ctl, sg, ia.B, ia.it, bid);
 }
 
 // ----------------------------------------------------------------------------
