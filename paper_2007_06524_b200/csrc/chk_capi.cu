@@ -114,6 +114,7 @@ template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 16, REG 
 template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2, REG = 0, RA = 1, P = 1; };
 
 // every h-cell inside its sub-cell (alpha = 1/2): stencil fast path
+// (n0 >= 4, checked by check_grid: every aligned x2 quad lies inside one cell)
 inline bool allin(const Geo& g) { return g.k == g.mask + 1 && g.off == 0; }
 
 template <int N>
@@ -326,8 +327,8 @@ int check_grid(const chk_grid* g, Geo* out) {
   if (!g) return fail(CHK_EINVAL, "grid is NULL");
   if (g->d != 3) return fail(CHK_EUNSUPPORTED, "only d = 3 is implemented on the GPU path");
   if (!supported_n(g->n)) return fail(CHK_EUNSUPPORTED, "n must be a power of two in [8, 512]");
-  if (g->n0 < 1 || (g->n0 & (g->n0 - 1)) || g->L < 1 || g->n0 * g->L != g->n)
-    return fail(CHK_EINVAL, "need n = n0 * L with n0 a power of two");
+  if (g->n0 < 4 || (g->n0 & (g->n0 - 1)) || g->L < 1 || g->n0 * g->L != g->n)  // lattice.py:122-123
+    return fail(CHK_EINVAL, "need n = n0 * L with n0 a power of two >= 4");
   if (g->k < 1 || g->k > g->n0 || g->offset < 0 || g->offset + g->k > g->n0)
     return fail(CHK_EINVAL, "sub-cell window outside the cell");
   if (!(g->lam > 0.0)) return fail(CHK_EINVAL, "lambda must be positive");

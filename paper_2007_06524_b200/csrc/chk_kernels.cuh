@@ -629,14 +629,6 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   }
 }
 
-template <int N, int G, int MODE, bool ALLIN>
-__global__ void __launch_bounds__(256) fwd_plane_kernel(Geo g, const double* __restrict__ beta,
-                                                        const double* __restrict__ src, double* __restrict__ u,
-                                                        double2* __restrict__ S, PlanDev pl,
-                                                        SolveCtl ctl, SlabGeo sg, int B, int it) {
-  fwd_plane_body<N, G, MODE, ALLIN>(g, beta, src, u, S, pl, ctl, sg, B, it, blockIdx.x);
-}
-
 // ----------------------------------------------------------------------------
 // kernel 2: spectral column pass (x1 group combine + x0), diagonal scaling
 // ----------------------------------------------------------------------------
@@ -1320,54 +1312,6 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
   }
 }
 
-template <int N, int G, int MODE>
-__global__ void __launch_bounds__(256) inv_plane_kernel(const double2* __restrict__ S,
-                                                        double* __restrict__ out, double* __restrict__ u,
-                                                        PlanDev pl, SolveCtl ctl, SlabGeo sg, int B, int it) {
-  inv_plane_body<N, G, MODE>(S, out, u, pl, ctl, sg, B, it, blockIdx.x);
-}
-
-// Paired plane pass: the forward pass of one half of the batch (q = A p, FFT;
-// fp64-pipe and latency heavy) and the inverse pass of the other half (iFFT,
-// u / p updates; HBM heavy) in ONE launch, their CTAs interleaved so that both
-// kinds are co-resident on every SM.  The two halves are half an iteration
-// apart (solver driver), so the launch has no internal dependency.
-struct FwdArgs {
-  Geo g;
-  const double* beta;
-  const double* p;
-  double* u;
-  double2* S;
-  SolveCtl ctl;
-  int B, it, blocks;
-};
-struct InvArgs {
-  const double2* S;
-  double* p;
-  double* u;
-  SolveCtl ctl;
-  int B, it, blocks;
-};
-
-template <int N, int G, bool ALLIN>
-__global__ void __launch_bounds__(256, 3) pair_plane_kernel(FwdArgs fa, InvArgs ia, PlanDev pl, SlabGeo sg) {
-  const int m = fa.blocks < ia.blocks ? fa.blocks : ia.blocks;
-  const int bx = blockIdx.x;
-  bool fwd;
-  int bid;
-  if (bx < 2 * m) {
-    fwd = (bx & 1) == 0;
-    bid = bx >> 1;
-  } else {
-    fwd = fa.blocks > m;
-    bid = bx - m;
-  }
-  if (fwd)
-    fwd_plane_body<N, G, FWD_Q, ALLIN>(fa.g, fa.beta, fa.p, fa.u, fa.S, pl, fa.ctl, sg, fa.B, fa.it, bid);
-  else
-    inv_plane_body<N, G, INV_ITER>(ia.S, ia.p, ia.u, pl, ia.ctl, sg, ia.B, ia.it, bid);
-}
-
 // ----------------------------------------------------------------------------
 // init / finalize reductions and the slab-mode decision kernels
 // ----------------------------------------------------------------------------
@@ -1487,3 +1431,5 @@ __global__ void decide_kernel(SolveCtl ctl, const double* __restrict__ red, int 
 }
 
 }  // namespace chk
+
+#include "chk_plane.cuh"

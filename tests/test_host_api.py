@@ -44,6 +44,10 @@ def test_abi_rejects_bad_arguments_without_gpu():
     assert lib.chk_precond_plan_create(7, 16, 5, None, None, 0.0, ctypes.byref(h)) == _lib.CHK_EINVAL
     g = _lib.ChkGrid(2, 16, 4, 4, 2, 1, 0.4)
     assert lib.chk_stencil_apply(ctypes.byref(g), None, None, None, None, 1, None) == _lib.CHK_EUNSUPPORTED
+    # n0 must be a power of two >= 4 (lattice.py:122-123); checked before any device work
+    g2 = _lib.ChkGrid(3, 16, 8, 2, 2, 0, 0.4)
+    assert lib.chk_stencil_apply(ctypes.byref(g2), None, None, None, None, 1, None) == _lib.CHK_EINVAL
+    assert b">= 4" in lib.chk_last_error()
     with pytest.raises(ValueError):
         _lib.check(_lib.CHK_EINVAL)
     assert lib.chk_pcg_workspace_bytes(ctypes.byref(g), None, 1, 10) == 0
