@@ -23,6 +23,13 @@
 #include "chk_fft.cuh"
 #include "chk_tma.cuh"
 
+#ifndef CHK_MID_RPF
+#define CHK_MID_RPF 1
+#endif
+#ifndef CHK_SC_FENCE
+#define CHK_SC_FENCE 0
+#endif
+
 namespace chk {
 
 enum : int { ST_CONVERGED = 0, ST_NOT_CONVERGED = 1, ST_BREAKDOWN = 2, ST_ACTIVE = 3 };
@@ -143,6 +150,16 @@ __device__ __forceinline__ int dig_freq(int p) {
 // ----------------------------------------------------------------------------
 // last-block reduction of two scalars per realization
 // ----------------------------------------------------------------------------
+// Release / acquire fences of the last-CTA ticket (message passing through
+// the partials); lighter than the sequentially consistent __threadfence().
+__device__ __forceinline__ void fence_release_gpu() {
+#if CHK_SC_FENCE
+  __threadfence();
+#else
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ bool reduce2_last(double v0, double v1, double* part, unsigned* cnt,
                                              int blk, int nblk, double* scratch, double& t0,
                                              double& t1) {
@@ -152,13 +169,13 @@ __device__ __forceinline__ bool reduce2_last(double v0, double v1, double* part,
   if (threadIdx.x == 0) {
     part[2 * blk] = v0;
     part[2 * blk + 1] = v1;
-    __threadfence();
+    fence_release_gpu();
     const unsigned prev = atomicAdd(cnt, 1u);
     s_last = (prev == (unsigned)(nblk - 1));
   }
   __syncthreads();
   if (!s_last) return false;
-  __threadfence();
+  fence_release_gpu();
   double a = 0.0, c = 0.0;
   for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
     a += __ldcg(part + 2 * i);
@@ -1022,7 +1039,18 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
       cp_async_commit();
     }
   };
+  // the residual tile of a realization (N x GW, contiguous) is read in phase B:
+  // pull it into L2 one realization ahead (the first one under the prologue)
+  auto prefetch_r = [&](int cc) {
+    if (MODE == MID_ITER && CHK_MID_RPF && threadIdx.x == 0 && cc < NB / P) {
+      for (int pr = 0; pr < P; ++pr)
+        if (s_act[cc * P + pr])
+          bulk_prefetch_l2(ctl.Rh + ((size_t)(b0 + cc * P + pr) * TILES + tile) * N * GW,
+                           (uint32_t)(N * GW * sizeof(double2)));
+    }
+  };
   stage(0);
+  prefetch_r(0);
   mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
 
   const double scale = 2.0 / ((double)N * N * N);
@@ -1107,6 +1135,7 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
     }
     __syncthreads();
     if (c + 1 < NB / P) stage(c + 1);  // overlaps phases B and A-inverse
+    prefetch_r(c + 1);
     // ---- phase B: remaining stages, residual update / diagonal, inverse ----
     double accr[P], accz[P];
 #pragma unroll
