@@ -44,9 +44,11 @@ struct Profiler {
     return e;
   }
   void collect() {  // call after the stream synchronized
+    static FILE* trace = getenv("CHK_PROF_TRACE") ? fopen(getenv("CHK_PROF_TRACE"), "a") : nullptr;
     for (auto& o : open) {
       float t = 0.f;
       if (cudaEventElapsedTime(&t, o.second.first, o.second.second) == cudaSuccess) {
+        if (trace) fprintf(trace, "%d %.5f\n", o.first, t);
         ms[o.first] += t;
         count[o.first] += 1;
       }
@@ -54,6 +56,7 @@ struct Profiler {
       pool.push_back(o.second.second);
     }
     open.clear();
+    if (trace) fflush(trace);
   }
 };
 thread_local Profiler g_prof;

@@ -81,6 +81,18 @@ struct SlabGeo {
   const double* halo_hi;  // [B][n*n] plane x0_off+nloc, null -> periodic inside p
 };
 
+// Interleaved spectrum layout (n = 256): a plane chunk is stored [ncols/W][G][W]
+// instead of [G][ncols], so that one x0 row of a middle-pass tile (W columns of
+// all G groups) is G*W*16 = 256 contiguous bytes, while a plane CTA writes / reads
+// W*16 = 32-byte pieces (whole DRAM sectors; the G CTAs of a plane run together).
+// Measured access patterns (tools/chunk_probe.cu): tile rows of 32 B 3.5 TB/s,
+// 256 B 6.3 TB/s; 32 B plane pieces 6.0 (write) / 5.6 (read) TB/s vs 7.4 contiguous.
+// 0 = the contiguous [G][ncols] layout.
+template <int N>
+struct IlW {
+  static constexpr int value = (N == 256) ? 2 : 0;
+};
+
 // start of the (s, b, x0l, g) row chunk of an exchange buffer (complex units)
 __host__ __device__ __forceinline__ size_t slab_row(const SlabGeo& sg, int B, int G, int s, int b, int x0l,
                                                     int g) {
@@ -551,6 +563,17 @@ __device__ __forceinline__ void ld4v(const double* p, double (&v)[4]) {
                : "l"(p));
 }
 
+__device__ __forceinline__ void ldv4(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p)
+               : "memory");
+}
+__device__ __forceinline__ void stv4(double* p, const double (&v)[4]) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+
 // CTA body, `bid` = plane block index (blockIdx.x of the stand-alone kernel)
 template <int N, int G, int MODE, bool ALLIN>
 __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __restrict__ beta,
@@ -637,6 +660,23 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   // (one bulk store each; a single chunk when the grid is not slab-decomposed)
   fence_proxy_async_smem();
   __syncthreads();
+  if constexpr (IlW<N>::value > 0) {
+    // interleaved layout: 32-byte pieces at a stride of G*W complex
+    constexpr int IW = IlW<N>::value;
+    static_assert(IW == 2, "piece copy assumes W = 2");
+    const int npc = sg.ncols / IW;
+    for (int c = 0; c < sg.P; ++c) {
+      double* dst = reinterpret_cast<double*>(S + slab_row(sg, B, G, c, b, x0l, 0) + gg * IW);
+      const double* src = reinterpret_cast<const double*>(buf + (size_t)c * sg.ncols);
+      for (int i = threadIdx.x; i < npc; i += blockDim.x) {
+        const double2 a = *reinterpret_cast<const double2*>(src + 4 * i);
+        const double2 d = *reinterpret_cast<const double2*>(src + 4 * i + 2);
+        const double v[4] = {a.x, a.y, d.x, d.y};
+        stv4(dst + (size_t)i * 2 * G * IW, v);
+      }
+    }
+    return;
+  }
   if (threadIdx.x < sg.P) {
     const int c = threadIdx.x;
     bulk_s2g(S + slab_row(sg, B, G, c, b, x0l, gg), buf + (size_t)c * sg.ncols,
@@ -862,6 +902,9 @@ __global__ void __launch_bounds__(256) mid_column_fused_kernel(double2* __restri
   constexpr int GW = G * W;
   constexpr int RS = GW + 1;
   constexpr int RL = LastRadix<N>::value;  // radix of the fused last x0 stage
+  constexpr bool IL = IlW<N>::value > 0;
+  static_assert(!IL || IlW<N>::value == W, "interleaved pieces are one tile wide");
+  const size_t GSTR = IL ? (size_t)W : (size_t)sg.ncols;  // stride between the groups of a column
   const int TILES = sg.tiles;
   const int nsh = __ffs(sg.nloc) - 1;
   extern __shared__ double2 buf[];
@@ -892,23 +935,46 @@ __global__ void __launch_bounds__(256) mid_column_fused_kernel(double2* __restri
   }
   __syncthreads();
   if (scratch[0] == 0.0) return;
+  // Pull realization jj's tile into L2 while the one before it is transformed:
+  // the N spectrum rows (G*W*16 contiguous bytes each with the interleaved
+  // layout) and the contiguous residual tile.
+  auto prefetch = [&](int jj) {
+    if (!IL || jj >= NB || !s_act[jj]) return;
+    const int bb = b0 + jj;
+    for (int x0 = threadIdx.x; x0 < N; x0 += blockDim.x)
+      bulk_prefetch_l2(S + slab_row(sg, B, G, x0 >> nsh, bb, x0 & (sg.nloc - 1), 0) + c0 * G,
+                       (uint32_t)(GW * sizeof(double2)));
+    if (MODE == MID_ITER && threadIdx.x == 0)
+      bulk_prefetch_l2(ctl.Rh + ((size_t)bb * TILES + tile) * N * GW, (uint32_t)(N * GW * sizeof(double2)));
+  };
+  {
+    int j0 = 0;
+    while (j0 < NB && !s_act[j0]) ++j0;
+    prefetch(j0);
+  }
   mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
   const double scale = 2.0 / ((double)N * N * N);
   for (int j = 0; j < NB; ++j) {
     if (!s_act[j]) continue;
     const int b = b0 + j;
     // ---- load + group combine (registers) -> smem ----
+#pragma unroll 2
     for (int item = threadIdx.x; item < N * W; item += blockDim.x) {
       const int w = item % W, x0 = item / W;
-      const size_t rbase = slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), 0) + c0 + w;
+      const size_t rbase = slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), 0) + (IL ? c0 * G : c0) + w;
       double2 v[G];
 #pragma unroll
-      for (int g = 0; g < G; ++g) v[g] = S[rbase + (size_t)g * sg.ncols];
+      for (int g = 0; g < G; ++g) v[g] = S[rbase + (size_t)g * GSTR];
 #pragma unroll
       for (int g = 1; g < G; ++g) v[g] = cmul(v[g], s_tw[g * W + w]);
       reg_fft<G, false>(v, pl.tw, N);
 #pragma unroll
       for (int g = 0; g < G; ++g) buf[x0 * RS + g * W + w] = v[g];
+    }
+    {
+      int jn = j + 1;
+      while (jn < NB && !s_act[jn]) ++jn;
+      prefetch(jn);
     }
     __syncthreads();
     FftRecButLast<N, N, false, GW>::run(buf, X0Addr{RS}, pl.tw, 1);
@@ -936,7 +1002,7 @@ __global__ void __launch_bounds__(256) mid_column_fused_kernel(double2* __restri
     // ---- inverse group combine + store (registers) ----
     for (int item = threadIdx.x; item < N * W; item += blockDim.x) {
       const int w = item % W, x0 = item / W;
-      const size_t rbase = slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), 0) + c0 + w;
+      const size_t rbase = slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), 0) + (IL ? c0 * G : c0) + w;
       double2 v[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) v[g] = buf[x0 * RS + g * W + w];
@@ -944,7 +1010,7 @@ __global__ void __launch_bounds__(256) mid_column_fused_kernel(double2* __restri
 #pragma unroll
       for (int g = 1; g < G; ++g) v[g] = cmulc(v[g], s_tw[g * W + w]);
 #pragma unroll
-      for (int g = 0; g < G; ++g) S[rbase + (size_t)g * sg.ncols] = v[g];
+      for (int g = 0; g < G; ++g) S[rbase + (size_t)g * GSTR] = v[g];
     }
     if (MODE != MID_APPLY) {
       RState* st = ctl.st + b;
@@ -1246,16 +1312,6 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
 //            (solver.py:184).  At the stopping iteration only u is updated.
 enum : int { INV_APPLY = 0, INV_INIT = 1, INV_ITER = 2 };
 
-__device__ __forceinline__ void ldv4(const double* p, double (&v)[4]) {
-  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
-               : "l"(p)
-               : "memory");
-}
-__device__ __forceinline__ void stv4(double* p, const double (&v)[4]) {
-  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
-               : "memory");
-}
 
 template <int N, int G, int MODE>
 __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, double* __restrict__ out,
@@ -1285,7 +1341,19 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     }
     if (!do_p && !do_u) return;
   }
-  if (do_p) {
+  constexpr int IW = IlW<N>::value;
+  if constexpr (IW > 0) {
+    if (do_p) {
+      // interleaved layout: 16-byte cp.async copies of the 32-byte pieces
+      for (int c = 0; c < sg.P; ++c) {
+        const double2* src = S + slab_row(sg, B, G, c, b, x0, 0) + gg * IW;
+        double2* dst = buf + (size_t)c * sg.ncols;
+        for (int i = threadIdx.x; i < sg.ncols; i += blockDim.x)
+          cp_async16(dst + i, src + (size_t)(i / IW) * G * IW + (i % IW));
+      }
+      cp_async_commit();
+    }
+  } else if (do_p) {
     // the slab row arrives as P column chunks (one bulk load each)
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
@@ -1302,8 +1370,13 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     bulk_prefetch_l2(u + ro, N * sizeof(double));
   }
   if (do_p) {
-    __syncthreads();  // barrier initialised before anyone waits
-    mbar_wait(&bar, 0);
+    if constexpr (IW > 0) {
+      cp_async_wait_all();
+      __syncthreads();
+    } else {
+      __syncthreads();  // barrier initialised before anyone waits
+      mbar_wait(&bar, 0);
+    }
     fft_smem<NR, true, H>(buf, ColAddr{HP}, pl.tw, N);
     c2r_pre<N>(buf, NR, HP, pl.tw);
     __syncthreads();
