@@ -157,23 +157,45 @@ struct Ops {
     return e;
   }
 
+  // plane-pass launch: 2-CTA clusters where the interleaved layout pairs groups (IlC)
+  template <class... KA, class... AA>
+  static cudaError_t plaunch(void (*kernel)(KA...), dim3 grid, size_t sm, cudaStream_t s, AA... args) {
+    if constexpr (IlC<N>::value > 1) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(PlaneNT<N>::value);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = IlC<N>::value;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, kernel, args...);
+    } else {
+      kernel<<<grid, PlaneNT<N>::value, sm, s>>>(args...);
+      return cudaSuccess;
+    }
+  }
   static int fwd(int mode, cudaStream_t s, int B, Geo g, const double* beta, const double* src,
                  double* u, double2* S, PlanDev pl, SolveCtl ctl, int it, SlabGeo sg = whole()) {
     const size_t sm = plane_smem();
-    dim3 grid(B * sg.nloc * G), block(256);
+    dim3 grid(B * sg.nloc * G);
     ProfScope ps(1, s);
     if (mode == FWD_APPLY) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_APPLY, false>, sm));
-      fwd_plane_kernel<N, G, FWD_APPLY, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, sg, B, it);
+      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_APPLY, false>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it));
     } else if (mode == FWD_INIT) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_INIT, false>, sm));
-      fwd_plane_kernel<N, G, FWD_INIT, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, sg, B, it);
+      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_INIT, false>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it));
     } else if (allin(g)) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_Q, true>, sm));
-      fwd_plane_kernel<N, G, FWD_Q, true><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, sg, B, it);
+      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_Q, true>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it));
     } else {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_Q, false>, sm));
-      fwd_plane_kernel<N, G, FWD_Q, false><<<grid, block, sm, s>>>(g, beta, src, u, S, pl, ctl, sg, B, it);
+      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_Q, false>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it));
     }
     CHK_LAUNCHED();
     return CHK_OK;
@@ -181,7 +203,7 @@ struct Ops {
   template <int NBX, int MODE>
   static int mid_launch(cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it, SlabGeo sg) {
     const int r1 = pl.kind == KIND_LKR ? pl.r1 : 0;
-    dim3 grid(((B + NBX - 1) / NBX) * sg.tiles), block(256);
+    dim3 grid(((B + NBX - 1) / NBX) * sg.tiles), block(PlaneNT<N>::value);
     if constexpr (REG) {
       constexpr int PX = (NBX == 1) ? 1 : P;
       constexpr int NT = (W * (N / RA) > 128 ? 256 : 128) * PX;
@@ -223,23 +245,24 @@ struct Ops {
   static int inv(int mode, cudaStream_t s, int B, const double2* S, double* out, double* u,
                  PlanDev pl, SolveCtl ctl, int it, SlabGeo sg = whole()) {
     const size_t sm = plane_smem();
-    dim3 grid(B * sg.nloc * G), block(256);
+    dim3 grid(B * sg.nloc * G);
     ProfScope ps(3, s);
     if (mode == INV_APPLY) {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_APPLY>, sm));
-      inv_plane_kernel<N, G, INV_APPLY><<<grid, block, sm, s>>>(S, out, u, pl, ctl, sg, B, it);
+      CHK_CUDA(plaunch(inv_plane_kernel<N, G, INV_APPLY>, grid, sm, s, S, out, u, pl, ctl, sg, B, it));
     } else if (mode == INV_INIT) {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_INIT>, sm));
-      inv_plane_kernel<N, G, INV_INIT><<<grid, block, sm, s>>>(S, out, u, pl, ctl, sg, B, it);
+      CHK_CUDA(plaunch(inv_plane_kernel<N, G, INV_INIT>, grid, sm, s, S, out, u, pl, ctl, sg, B, it));
     } else {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_ITER>, sm));
-      inv_plane_kernel<N, G, INV_ITER><<<grid, block, sm, s>>>(S, out, u, pl, ctl, sg, B, it);
+      CHK_CUDA(plaunch(inv_plane_kernel<N, G, INV_ITER>, grid, sm, s, S, out, u, pl, ctl, sg, B, it));
     }
     CHK_LAUNCHED();
     return CHK_OK;
   }
   // paired plane pass (pair_plane_kernel): fa.blocks forward + ia.blocks inverse CTAs
   static int pair(cudaStream_t s, const FwdArgs& fa, const InvArgs& ia, PlanDev pl) {
+    if constexpr (IlC<N>::value > 1) return fail(CHK_EUNSUPPORTED, "paired plane pass with clustered plane CTAs");
     const size_t sm = plane_smem();
     const SlabGeo sg = whole();
     dim3 grid(fa.blocks + ia.blocks), block(256);

@@ -23,6 +23,9 @@
 #include "chk_fft.cuh"
 #include "chk_tma.cuh"
 
+#ifndef CHK_FUSED_PF  // L2 prefetch of the next realization in the fused middle pass
+#define CHK_FUSED_PF 0
+#endif
 #ifndef CHK_MID_RPF
 #define CHK_MID_RPF 1
 #endif
@@ -81,16 +84,42 @@ struct SlabGeo {
   const double* halo_hi;  // [B][n*n] plane x0_off+nloc, null -> periodic inside p
 };
 
-// Interleaved spectrum layout (n = 256): a plane chunk is stored [ncols/W][G][W]
+// Interleaved spectrum layout (n >= 256): a plane chunk is stored [ncols/W][G][W]
 // instead of [G][ncols], so that one x0 row of a middle-pass tile (W columns of
-// all G groups) is G*W*16 = 256 contiguous bytes, while a plane CTA writes / reads
-// W*16 = 32-byte pieces (whole DRAM sectors; the G CTAs of a plane run together).
-// Measured access patterns (tools/chunk_probe.cu): tile rows of 32 B 3.5 TB/s,
-// 256 B 6.3 TB/s; 32 B plane pieces 6.0 (write) / 5.6 (read) TB/s vs 7.4 contiguous.
-// 0 = the contiguous [G][ncols] layout.
+// all G groups) is G*W*16 = 256 contiguous bytes, while the plane passes move
+// pieces of IlC*W*16 = 32 bytes (whole DRAM sectors; the G CTAs of a plane run
+// together).  n = 256: W = 2, each CTA moves its own pieces.  n = 512: W = 1, the
+// CTAs of groups (2h, 2h+1) form a 2-CTA cluster and each moves the 32-byte
+// pieces of both groups for half of the columns, exchanging the other group's
+// half through distributed shared memory (16-byte pieces would cost a
+// read-modify-write per sector).  Measured access patterns
+// (tools/chunk_probe.cu): tile rows of 16 B 2.3 TB/s, 32 B 3.5 TB/s, 256 B
+// 6.3 TB/s; 32 B plane pieces 6.0 (write) / 5.6 (read) TB/s vs 7.4 contiguous,
+// 16 B pieces 1.1 / 3.5 TB/s.  IlW = 0: the contiguous [G][ncols] layout.
+// n = 512 default: contiguous layout (CHK_IL512=0).  Measured on config 5 with 512
+// threads per CTA: the clustered interleaved layout speeds the middle pass up by
+// only 5 % (it runs one CTA per SM, latency-bound) while the cluster barriers and
+// synchronous piece loads slow the plane passes by 17 % / 38 % (2.11e10 vs
+// 2.28e10 DOF-it/s); the clustered path stays selectable for experiments.
+#ifndef CHK_IL512
+#define CHK_IL512 0
+#endif
+#ifndef CHK_NT512
+#define CHK_NT512 512
+#endif
 template <int N>
 struct IlW {
-  static constexpr int value = (N == 256) ? 2 : 0;
+  static constexpr int value = (N == 256) ? 2 : ((N == 512 && CHK_IL512) ? 1 : 0);
+};
+// threads per CTA of the plane passes and the fused middle pass: n = 512 runs one
+// CTA per SM (131 KB slab), so it takes more warps per CTA
+template <int N>
+struct PlaneNT {
+  static constexpr int value = (N == 512) ? CHK_NT512 : 256;
+};
+template <int N>
+struct IlC {  // CTAs per cluster of the plane passes
+  static constexpr int value = (N == 512 && CHK_IL512) ? 2 : 1;
 };
 
 // start of the (s, b, x0l, g) row chunk of an exchange buffer (complex units)
@@ -662,18 +691,40 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   __syncthreads();
   if constexpr (IlW<N>::value > 0) {
     // interleaved layout: 32-byte pieces at a stride of G*W complex
-    constexpr int IW = IlW<N>::value;
-    static_assert(IW == 2, "piece copy assumes W = 2");
-    const int npc = sg.ncols / IW;
-    for (int c = 0; c < sg.P; ++c) {
-      double* dst = reinterpret_cast<double*>(S + slab_row(sg, B, G, c, b, x0l, 0) + gg * IW);
-      const double* src = reinterpret_cast<const double*>(buf + (size_t)c * sg.ncols);
-      for (int i = threadIdx.x; i < npc; i += blockDim.x) {
-        const double2 a = *reinterpret_cast<const double2*>(src + 4 * i);
-        const double2 d = *reinterpret_cast<const double2*>(src + 4 * i + 2);
-        const double v[4] = {a.x, a.y, d.x, d.y};
-        stv4(dst + (size_t)i * 2 * G * IW, v);
+    constexpr int IW = IlW<N>::value, CL = IlC<N>::value;
+    static_assert(IW * CL == 2, "pieces are two complex values");
+    if constexpr (CL == 1) {
+      const int npc = sg.ncols / IW;
+      for (int c = 0; c < sg.P; ++c) {
+        double* dst = reinterpret_cast<double*>(S + slab_row(sg, B, G, c, b, x0l, 0) + gg * IW);
+        const double* src = reinterpret_cast<const double*>(buf + (size_t)c * sg.ncols);
+        for (int i = threadIdx.x; i < npc; i += blockDim.x) {
+          const double2 a = *reinterpret_cast<const double2*>(src + 4 * i);
+          const double2 d = *reinterpret_cast<const double2*>(src + 4 * i + 2);
+          const double v[4] = {a.x, a.y, d.x, d.y};
+          stv4(dst + (size_t)i * 2 * G * IW, v);
+        }
       }
+    } else {
+      // 2-CTA cluster (groups g0, g0 + 1): this CTA stores columns [r*h, (r+1)*h) of both
+      cluster_sync_all();  // both slabs complete
+      const int r = (int)cluster_rank();
+      const int g0 = gg - r;
+      const uint32_t other = dsmem_map(buf, (uint32_t)(r ^ 1));
+      const int h = sg.ncols / 2;
+      for (int c = 0; c < sg.P; ++c) {
+        double* dst = reinterpret_cast<double*>(S + slab_row(sg, B, G, c, b, x0l, 0) + g0);
+#pragma unroll 4
+        for (int i = r * h + threadIdx.x; i < (r + 1) * h; i += blockDim.x) {
+          const int e = c * sg.ncols + i;
+          const double2 mine = buf[e];
+          const double2 theirs = dsmem_ld2(other + (uint32_t)e * 16u);
+          const double2 lo = r ? theirs : mine, hi = r ? mine : theirs;
+          const double v[4] = {lo.x, lo.y, hi.x, hi.y};
+          stv4(dst + (size_t)i * 2 * G, v);
+        }
+      }
+      cluster_sync_all();  // the partner has read this CTA's slab
     }
     return;
   }
@@ -894,7 +945,7 @@ __device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restri
 // inverse stage] in registers, remaining inverse stages, inverse group combine
 // + store in registers: 12 shared-memory passes per element instead of 20.
 template <int N, int G, int W, int NB, int MODE>
-__global__ void __launch_bounds__(256) mid_column_fused_kernel(double2* __restrict__ S, PlanDev pl,
+__global__ void __launch_bounds__(PlaneNT<N>::value) mid_column_fused_kernel(double2* __restrict__ S, PlanDev pl,
                                                                SolveCtl ctl, SlabGeo sg, int it, int B) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
@@ -939,7 +990,7 @@ __global__ void __launch_bounds__(256) mid_column_fused_kernel(double2* __restri
   // the N spectrum rows (G*W*16 contiguous bytes each with the interleaved
   // layout) and the contiguous residual tile.
   auto prefetch = [&](int jj) {
-    if (!IL || jj >= NB || !s_act[jj]) return;
+    if (!IL || !CHK_FUSED_PF || jj >= NB || !s_act[jj]) return;
     const int bb = b0 + jj;
     for (int x0 = threadIdx.x; x0 < N; x0 += blockDim.x)
       bulk_prefetch_l2(S + slab_row(sg, B, G, x0 >> nsh, bb, x0 & (sg.nloc - 1), 0) + c0 * G,
@@ -1341,8 +1392,8 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     }
     if (!do_p && !do_u) return;
   }
-  constexpr int IW = IlW<N>::value;
-  if constexpr (IW > 0) {
+  constexpr int IW = IlW<N>::value, CL = IlC<N>::value;
+  if constexpr (IW > 0 && CL == 1) {
     if (do_p) {
       // interleaved layout: 16-byte cp.async copies of the 32-byte pieces
       for (int c = 0; c < sg.P; ++c) {
@@ -1352,6 +1403,29 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
           cp_async16(dst + i, src + (size_t)(i / IW) * G * IW + (i % IW));
       }
       cp_async_commit();
+    }
+  } else if constexpr (IW > 0) {
+    static_assert(IW == 1 && CL == 2, "cluster pieces: two groups of one column");
+    if (do_p) {  // uniform over the cluster (one realization)
+      // 2-CTA cluster: this CTA loads the 32-byte pieces (both groups) of columns
+      // [r*h, (r+1)*h) and delivers the partner's group through DSMEM
+      cluster_sync_all();  // the partner is running (its window may be written)
+      const int r = (int)cluster_rank();
+      const int g0 = gg - r;
+      const uint32_t other = dsmem_map(buf, (uint32_t)(r ^ 1));
+      const int h = sg.ncols / 2;
+      for (int c = 0; c < sg.P; ++c) {
+        const double* src = reinterpret_cast<const double*>(S + slab_row(sg, B, G, c, b, x0, 0) + g0);
+#pragma unroll 4
+        for (int i = r * h + threadIdx.x; i < (r + 1) * h; i += blockDim.x) {
+          double v[4];
+          ldv4(src + (size_t)i * 2 * G, v);
+          const int e = c * sg.ncols + i;
+          const double2 lo = make_double2(v[0], v[1]), hi = make_double2(v[2], v[3]);
+          buf[e] = r ? hi : lo;
+          dsmem_st2(other + (uint32_t)e * 16u, r ? lo : hi);
+        }
+      }
     }
   } else if (do_p) {
     // the slab row arrives as P column chunks (one bulk load each)
@@ -1370,9 +1444,11 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     bulk_prefetch_l2(u + ro, N * sizeof(double));
   }
   if (do_p) {
-    if constexpr (IW > 0) {
+    if constexpr (IW > 0 && CL == 1) {
       cp_async_wait_all();
       __syncthreads();
+    } else if constexpr (IW > 0) {
+      cluster_sync_all();  // both halves delivered
     } else {
       __syncthreads();  // barrier initialised before anyone waits
       mbar_wait(&bar, 0);
