@@ -203,7 +203,7 @@ struct Ops {
   template <int NBX, int MODE>
   static int mid_launch(cudaStream_t s, int B, double2* S, PlanDev pl, SolveCtl ctl, int it, SlabGeo sg) {
     const int r1 = pl.kind == KIND_LKR ? pl.r1 : 0;
-    dim3 grid(((B + NBX - 1) / NBX) * sg.tiles), block(PlaneNT<N>::value);
+    dim3 grid(((B + NBX - 1) / NBX) * sg.tiles), block(MidNT<N>::value);
     if constexpr (REG) {
       constexpr int PX = (NBX == 1) ? 1 : P;
       constexpr int NT = (W * (N / RA) > 128 ? 256 : 128) * PX;

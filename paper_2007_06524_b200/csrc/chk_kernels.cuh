@@ -113,9 +113,17 @@ struct IlW {
 };
 // threads per CTA of the plane passes and the fused middle pass: n = 512 runs one
 // CTA per SM (131 KB slab), so it takes more warps per CTA
+// (n = 256: 512-thread CTAs measured slower -- 64 registers spill -- for both.)
+// The fused middle pass states its 2 CTAs per SM at n <= 256 (<= 128 registers):
+// an explicit minimum of 1 lets nvcc take 164 registers and halves occupancy.
 template <int N>
 struct PlaneNT {
   static constexpr int value = (N == 512) ? CHK_NT512 : 256;
+};
+template <int N>
+struct MidNT {
+  static constexpr int value = (N == 512) ? CHK_NT512 : 256;
+  static constexpr int minb = (N == 512) ? 1 : 2;
 };
 template <int N>
 struct IlC {  // CTAs per cluster of the plane passes
@@ -945,7 +953,7 @@ __device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restri
 // inverse stage] in registers, remaining inverse stages, inverse group combine
 // + store in registers: 12 shared-memory passes per element instead of 20.
 template <int N, int G, int W, int NB, int MODE>
-__global__ void __launch_bounds__(PlaneNT<N>::value) mid_column_fused_kernel(double2* __restrict__ S, PlanDev pl,
+__global__ void __launch_bounds__(MidNT<N>::value, MidNT<N>::minb) mid_column_fused_kernel(double2* __restrict__ S, PlanDev pl,
                                                                SolveCtl ctl, SlabGeo sg, int it, int B) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
