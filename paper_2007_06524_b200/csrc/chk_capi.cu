@@ -122,6 +122,7 @@ inline bool allin(const Geo& g) { return g.k == g.mask + 1 && g.off == 0; }
 
 template <int N>
 struct Ops {
+  static constexpr int NN = N;
   static constexpr int G = Cfg<N>::G, W = Cfg<N>::W, NB = Cfg<N>::NB, NR = N / G, H = N / 2 + 1;
   static constexpr int REG = Cfg<N>::REG, RA = Cfg<N>::RA, P = Cfg<N>::P;
 #ifndef CHK_STAGE
@@ -425,10 +426,11 @@ struct chk_precond_plan {
   double* d_U;
   double* d_Up;
   double* d_lam;
+  double* d_D;  // [tiles][n][G*W] diagonal tiles, computed once at plan creation
 };
 
 static PlanDev plan_dev(const chk_precond_plan* p) {
-  return PlanDev{p->d_tw, p->d_U, p->d_Up, p->d_lam, p->r1, p->kind, p->delta};
+  return PlanDev{p->d_tw, p->d_U, p->d_Up, p->d_lam, p->r1, p->kind, p->delta, p->d_D};
 }
 
 // host copy of dig_freq (chk_kernels.cuh): frequency stored at digit-reversed position p
@@ -444,6 +446,24 @@ static int host_dig_freq(int N, int p) {
     M = Mn;
   }
   return k;
+}
+
+// Evaluate every diagonal tile of a plan into p->d_D (dtile_kernel).
+static int plan_dtiles(chk_precond_plan* p) {
+  const int n = p->n;
+  const size_t nd = (size_t)n * n * (n / 2 + 1);
+  CHK_CUDA(cudaMalloc(&p->d_D, sizeof(double) * nd));
+  PlanDev pl = plan_dev(p);
+  pl.D = nullptr;
+  CHK_DISPATCH(n, {
+    constexpr int GW = O::G * O::W;
+    const size_t sm = sizeof(double) * (((size_t)p->r1 * GW + 1) / 2 * 2 + (size_t)n * GW);
+    CHK_CUDA(O::allow_smem(dtile_kernel<O::NN, O::G, O::W>, sm));
+    dtile_kernel<O::NN, O::G, O::W><<<O::TILES, 256, sm>>>(pl, p->d_D);
+    CHK_LAUNCHED();
+  });
+  CHK_CUDA(cudaDeviceSynchronize());
+  return CHK_OK;
 }
 
 extern "C" {
@@ -483,7 +503,8 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
   if (kind != CHK_PRECOND_LKR && eigenvalues == nullptr)
     return fail(CHK_EINVAL, "Fourier plans need the eigenvalues");
   if (kind == CHK_PRECOND_REGULARIZED && delta < 0.0) return fail(CHK_EINVAL, "delta must be >= 0");
-  auto* p = new chk_precond_plan{kind, n, kind == CHK_PRECOND_LKR ? r1 : 0, delta, nullptr, nullptr, nullptr, nullptr};
+  auto* p = new chk_precond_plan{kind, n, kind == CHK_PRECOND_LKR ? r1 : 0, delta, nullptr, nullptr, nullptr, nullptr,
+                                 nullptr};
   // twiddles w[k] = exp(-2 pi i k / n), octant-reduced for symmetric accuracy
   std::vector<double2> tw(n);
   for (int k = 0; k < n; ++k) {
@@ -515,6 +536,15 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
     if ((e = cudaMalloc(&p->d_lam, sizeof(double) * n)) != cudaSuccess) goto cuda_fail;
     if ((e = cudaMemcpy(p->d_lam, eigenvalues, sizeof(double) * n, cudaMemcpyHostToDevice)) != cudaSuccess) goto cuda_fail;
   }
+  // diagonal tiles of every middle-pass tile (n^2 (n/2+1) doubles: 8.5 MB at
+  // n = 128, 539 MB at n = 512); CHK_NO_DTILE=1 evaluates them per CTA instead
+  if (!(getenv("CHK_NO_DTILE") && atoi(getenv("CHK_NO_DTILE")))) {
+    const int rc2 = plan_dtiles(p);
+    if (rc2) {
+      chk_precond_plan_destroy(p);
+      return rc2;
+    }
+  }
   *out = p;
   return CHK_OK;
 cuda_fail:
@@ -528,6 +558,7 @@ int32_t chk_precond_plan_destroy(chk_precond_plan* p) {
   if (p->d_U) cudaFree(p->d_U);
   if (p->d_Up) cudaFree(p->d_Up);
   if (p->d_lam) cudaFree(p->d_lam);
+  if (p->d_D) cudaFree(p->d_D);
   delete p;
   return CHK_OK;
 }

@@ -158,6 +158,7 @@ struct PlanDev {
   int r1;
   int kind;
   double delta;
+  const double* D;    // [tiles][n][G*W] precomputed diagonal tiles (chk_dtile_kernel), or null
 };
 
 // ----------------------------------------------------------------------------
@@ -209,12 +210,35 @@ __device__ __forceinline__ void fence_release_gpu() {
 #endif
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Sum of the nblk partial pairs of a realization by its last CTA (after the
+// ticket): fixed order, result valid in every thread.  scratch >= 64 doubles.
+__device__ __forceinline__ void last_sum2(const double* part, int nblk, double* scratch, double& t0,
+                                          double& t1) {
+  fence_release_gpu();
+  double a = 0.0, c = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    a += __ldcg(part + 2 * i);
+    c += __ldcg(part + 2 * i + 1);
+  }
+  block_sum2(a, c, scratch);
+  t0 = a;
+  t1 = c;
+}
+
+// Per-CTA partial (v0, v1) of a realization -> part[blk]; true in the CTA that
+// took the last ticket, with the totals in t0 / t1 (every thread).
+// scratch >= 64 doubles.
 __device__ __forceinline__ bool reduce2_last(double v0, double v1, double* part, unsigned* cnt,
                                              int blk, int nblk, double* scratch, double& t0,
                                              double& t1) {
   __shared__ int s_last;
-  v0 = block_sum(v0, scratch);
-  v1 = block_sum(v1, scratch);
+  block_sum2(v0, v1, scratch);
   if (threadIdx.x == 0) {
     part[2 * blk] = v0;
     part[2 * blk + 1] = v1;
@@ -224,16 +248,64 @@ __device__ __forceinline__ bool reduce2_last(double v0, double v1, double* part,
   }
   __syncthreads();
   if (!s_last) return false;
-  fence_release_gpu();
-  double a = 0.0, c = 0.0;
-  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
-    a += __ldcg(part + 2 * i);
-    c += __ldcg(part + 2 * i + 1);
-  }
-  t0 = block_sum(a, scratch);
-  t1 = block_sum(c, scratch);
+  last_sum2(part, nblk, scratch, t0, t1);
   if (threadIdx.x == 0) *cnt = 0u;
   return true;
+}
+
+// Deferred form for CTAs that process several realizations: per realization j
+// each warp leaves its shuffle sums in wsum[j][warp][2] (warp_partials, no
+// barrier); after the last realization (and a __syncthreads) mid_tickets folds
+// them in the fixed order of block_sum2, publishes the partials, takes one
+// ticket per realization (one fence per writer instead of one per
+// realization) and runs the decisions of the realizations whose last CTA this
+// is.  Same sums, same order as reduce2_last.
+// wsum: [NB][warps per CTA][2]
+__device__ __forceinline__ void warp_partials(double v0, double v1, double* wsum, int j) {
+  v0 = warp_sum(v0);
+  v1 = warp_sum(v1);
+  if ((threadIdx.x & 31) == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    wsum[2 * (j * nw + (threadIdx.x >> 5))] = v0;
+    wsum[2 * (j * nw + (threadIdx.x >> 5)) + 1] = v1;
+  }
+}
+template <int NB, class Decide>
+__device__ __forceinline__ void mid_tickets(const double* wsum, const int* act, int b0, int blk,
+                                            int nblk, const SolveCtl& ctl, double* scratch, Decide decide) {
+  __shared__ int s_last[NB];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  for (int j = wid; j < NB; j += nw) {
+    int last = 0;
+    if (act[j]) {
+      double a = (lane < nw) ? wsum[2 * (j * nw + lane)] : 0.0;
+      double c = (lane < nw) ? wsum[2 * (j * nw + lane) + 1] : 0.0;
+      a = warp_sum(a);
+      c = warp_sum(c);
+      if (lane == 0) {
+        const int b = b0 + j;
+        double* part = ctl.part + (size_t)b * 2 * ctl.maxblk;
+        part[2 * blk] = a;
+        part[2 * blk + 1] = c;
+        fence_release_gpu();
+        const unsigned prev = atomicAdd(&ctl.st[b].cnt, 1u);
+        last = (prev == (unsigned)(nblk - 1));
+      }
+    }
+    if (lane == 0) s_last[j] = last;
+  }
+  __syncthreads();
+  for (int j = 0; j < NB; ++j) {
+    if (!s_last[j]) continue;
+    const int b = b0 + j;
+    double t0, t1;
+    last_sum2(ctl.part + (size_t)b * 2 * ctl.maxblk, nblk, scratch, t0, t1);
+    if (threadIdx.x == 0) {
+      ctl.st[b].cnt = 0u;
+      decide(b, t0, t1);
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -444,7 +516,7 @@ __global__ void __launch_bounds__(256) stencil_apply_kernel(Geo g, const double*
                                                             double* __restrict__ y, double* xy,
                                                             double* part, unsigned* cnt) {
   constexpr int NR = N / G;
-  __shared__ double scratch[32];
+  __shared__ double scratch[64];
   const int b = blockIdx.x / (N * G);
   const int rem = blockIdx.x - b * (N * G);
   const int x0 = rem / G, gg = rem - (rem / G) * G;
@@ -623,7 +695,7 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   constexpr int H = N2 + 1;
   constexpr int HP = H;
   extern __shared__ double2 buf[];
-  __shared__ double scratch[32];
+  __shared__ double scratch[64];
   const int nlg = sg.nloc * G;
   const int b = bid / nlg;
   const int rem = bid - b * nlg;
@@ -811,10 +883,10 @@ __device__ __forceinline__ void mid_decide(RState* st, const SolveCtl& ctl, int 
   }
 }
 
-// Shared prologue of both middle kernels: slot bookkeeping and the diagonal tile.
-template <int N, int G, int W, int MODE>
-__device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, const PlanDev& pl,
-                                             int* s_k1, int* s_k2, double* s_wgt, double2* s_tw, int dbg = 0) {
+// Slot bookkeeping of a middle-pass tile starting at global column c0.
+template <int N, int G, int W>
+__device__ __forceinline__ void mid_slots(int c0, const PlanDev& pl, int* s_k1, int* s_k2, double* s_wgt,
+                                          double2* s_tw) {
   constexpr int NR = N / G, N2 = N / 2, H = N2 + 1, GW = G * W;
   for (int s = threadIdx.x; s < GW; s += blockDim.x) {
     const int m = dig_freq<G>(s / W), w = s % W;
@@ -825,13 +897,19 @@ __device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, 
     const int k2 = (q2 == N2) ? N2 : dig_freq<N2>(q2);
     s_k2[s] = k2;
     s_wgt[s] = (k2 == 0 || k2 == N2) ? 1.0 : 2.0;
-    s_tw[s] = __ldg(pl.tw + (s / W) * kp);  // as a load slot (group s/W, column w)
+    if (s_tw) s_tw[s] = __ldg(pl.tw + (s / W) * kp);  // as a load slot (group s/W, column w)
   }
-  __syncthreads();
-  if (dbg & 16) return;  // timing experiment: no diagonal tile
+}
+
+// The diagonal tile D[pos0][slot] (x0 in digit-reversed order) of the
+// preconditioner, evaluated from its factors (slots from mid_slots, synced).
+// `coef` is scratch of r1 * G*W doubles.
+template <int N, int G, int W>
+__device__ __forceinline__ void mid_dtile(double* coef, double* Dsm, const PlanDev& pl, const int* s_k1,
+                                          const int* s_k2) {
+  constexpr int GW = G * W;
   if (pl.kind == KIND_LKR) {
-    // D = U0p^T C, C[r][slot] = U1[r][k1] U2[r][k2]: rank-r1 contraction, once per CTA
-    double* coef = reinterpret_cast<double*>(buf);
+    // D = U0p^T C, C[r][slot] = U1[r][k1] U2[r][k2]: rank-r1 contraction
     const double* U1 = pl.U + (size_t)pl.r1 * N;
     const double* U2 = pl.U + (size_t)2 * pl.r1 * N;
     for (int i = threadIdx.x; i < pl.r1 * GW; i += blockDim.x) {
@@ -882,6 +960,46 @@ __device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, 
       }
       Dsm[pos0 * GW + s] = D;
     }
+  }
+}
+
+// Precompute of every diagonal tile of a plan (once per plan; the middle
+// passes then stream their tile from HBM instead of re-evaluating the rank-r1
+// contraction per CTA).  CTA = tile; smem: r1 * GW + N * GW doubles.
+template <int N, int G, int W>
+__global__ void __launch_bounds__(256) dtile_kernel(PlanDev pl, double* __restrict__ Dout) {
+  constexpr int GW = G * W;
+  extern __shared__ double dsh[];
+  __shared__ int s_k1[GW], s_k2[GW];
+  __shared__ double s_wgt[GW];
+  const int r1 = pl.kind == KIND_LKR ? pl.r1 : 0;
+  double* coef = dsh;
+  double* Dsm = dsh + ((r1 * GW + 1) & ~1);
+  mid_slots<N, G, W>(blockIdx.x * W, pl, s_k1, s_k2, s_wgt, nullptr);
+  __syncthreads();
+  mid_dtile<N, G, W>(coef, Dsm, pl, s_k1, s_k2);
+  __syncthreads();
+  double* out = Dout + (size_t)blockIdx.x * N * GW;
+  for (int i = threadIdx.x; i < N * GW; i += blockDim.x) out[i] = Dsm[i];
+}
+
+// Shared prologue of both middle kernels: slot bookkeeping and the diagonal
+// tile (16-byte async copies of the precomputed tile, or evaluated in place).
+template <int N, int G, int W, int MODE>
+__device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, const PlanDev& pl,
+                                             int* s_k1, int* s_k2, double* s_wgt, double2* s_tw, int dbg = 0) {
+  constexpr int GW = G * W;
+  mid_slots<N, G, W>(c0, pl, s_k1, s_k2, s_wgt, s_tw);
+  if (pl.D) {
+    const double* src = pl.D + (size_t)(c0 / W) * N * GW;
+    for (int i = threadIdx.x; i < N * GW / 2; i += blockDim.x) cp_async16(Dsm + 2 * i, src + 2 * i);
+    cp_async_commit();
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  if (dbg & 16) return;  // timing experiment: no diagonal tile
+  if (!pl.D) {
+    mid_dtile<N, G, W>(reinterpret_cast<double*>(buf), Dsm, pl, s_k1, s_k2);
   }
   __syncthreads();
   if (MODE != MID_APPLY && threadIdx.x < GW) {
@@ -969,12 +1087,13 @@ __global__ void __launch_bounds__(MidNT<N>::value, MidNT<N>::minb) mid_column_fu
   extern __shared__ double2 buf[];
   const int doff = mid_dsm_offset(N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
   double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
-  __shared__ double scratch[32];
+  __shared__ double scratch[64];
   __shared__ int s_k1[GW], s_k2[GW];
   __shared__ double s_wgt[GW];
   __shared__ double2 s_tw[GW];
   __shared__ int s_act[NB];
   __shared__ double s_alpha[NB];
+  __shared__ double s_wsum[NB * (MidNT<N>::value / 32) * 2];  // per-warp Parseval partials (warp_partials)
   const int bg = blockIdx.x / TILES;
   const int tile = blockIdx.x - bg * TILES;
   const int c0 = tile * W;
@@ -1071,17 +1190,14 @@ __global__ void __launch_bounds__(MidNT<N>::value, MidNT<N>::minb) mid_column_fu
 #pragma unroll
       for (int g = 0; g < G; ++g) S[rbase + (size_t)g * GSTR] = v[g];
     }
-    if (MODE != MID_APPLY) {
-      RState* st = ctl.st + b;
-      double t0, t1;
-      if (reduce2_last(rr, rz, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile, TILES,
-                       scratch, t0, t1)) {
-        const double inv = 1.0 / ((double)N * N * N);  // Parseval: (1/N^3) sum conj(X) Y
-        if (threadIdx.x == 0) mid_decide(st, ctl, b, it, t0 * inv, t1 * inv);
-      }
-    } else {
-      __syncthreads();
-    }
+    if (MODE != MID_APPLY) warp_partials(rr, rz, s_wsum, j);
+    __syncthreads();
+  }
+  if (MODE != MID_APPLY) {
+    const double inv = 1.0 / ((double)N * N * N);  // Parseval: (1/N^3) sum conj(X) Y
+    mid_tickets<NB>(s_wsum, s_act, b0, tile, TILES, ctl, scratch, [&](int b, double t0, double t1) {
+      mid_decide(ctl.st + b, ctl, b, it, t0 * inv, t1 * inv);
+    });
   }
 }
 
@@ -1095,11 +1211,6 @@ __global__ void __launch_bounds__(MidNT<N>::value, MidNT<N>::minb) mid_column_fu
 // residual update / diagonal scaling and the inverse stages in registers.
 // Shared memory is touched twice per element per direction (one exchange each
 // way).  P realizations are in flight per CTA; NB share one diagonal tile.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 template <int N, int G, int W, int RA, int NB, int P, int MODE, int NT, bool STG = false>
 __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kernel(double2* __restrict__ S, PlanDev pl,
@@ -1120,12 +1231,13 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
   extern __shared__ double2 buf[];  // [P][N][RS] (aliased by the [r1][GW] coefficients)
   const int doff = mid_dsm_offset(P * N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
   double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
-  __shared__ double scratch[32];
+  __shared__ double scratch[64];
   __shared__ int s_k1[GW], s_k2[GW];
   __shared__ double s_wgt[GW];
   __shared__ double2 s_tw[GW];
   __shared__ int s_act[NB];
   __shared__ double s_alpha[NB];
+  __shared__ double s_wsum[NB * (NT / 32) * 2];  // per-warp Parseval partials (warp_partials)
   const int bg = blockIdx.x / TILES;
   const int tile = blockIdx.x - bg * TILES;
   const int c0 = tile * W;                       // first column inside this rank's chunk
@@ -1343,22 +1455,19 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
         }
       }
     }
-    // ---- per-realization Parseval reductions and decisions ----
+    // ---- per-realization Parseval partials (warp level; tickets after the loop) ----
     if (MODE != MID_APPLY) {
 #pragma unroll
-      for (int pr = 0; pr < P; ++pr) {
-        const int b = b0 + c * P + pr;
-        if (!s_act[c * P + pr]) continue;
-        RState* st = ctl.st + b;
-        double t0, t1;
-        if (reduce2_last(accr[pr], accz[pr], ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, tile,
-                         TILES, scratch, t0, t1)) {
-          const double inv = 1.0 / ((double)N * N * N);
-          if (threadIdx.x == 0) mid_decide(st, ctl, b, it, t0 * inv, t1 * inv);
-        }
-      }
+      for (int pr = 0; pr < P; ++pr)
+        if (s_act[c * P + pr]) warp_partials(accr[pr], accz[pr], s_wsum, c * P + pr);
     }
     __syncthreads();
+  }
+  if (MODE != MID_APPLY) {
+    const double inv = 1.0 / ((double)N * N * N);  // Parseval: (1/N^3) sum conj(X) Y
+    mid_tickets<NB>(s_wsum, s_act, b0, tile, TILES, ctl, scratch, [&](int b, double t0, double t1) {
+      mid_decide(ctl.st + b, ctl, b, it, t0 * inv, t1 * inv);
+    });
   }
 }
 
@@ -1523,7 +1632,7 @@ __device__ __forceinline__ void stats_decide(RState* st, double sum, double sums
 template <int N, int G>
 __global__ void __launch_bounds__(256) rhs_stats_kernel(const double* __restrict__ f, SolveCtl ctl, SlabGeo sg) {
   constexpr int NR = N / G;
-  __shared__ double scratch[32];
+  __shared__ double scratch[64];
   const int nlg = sg.nloc * G;
   const int b = blockIdx.x / nlg;
   const int rem = blockIdx.x - b * nlg;
@@ -1554,7 +1663,7 @@ __global__ void __launch_bounds__(256) rhs_stats_kernel(const double* __restrict
 template <int N, int G>
 __global__ void __launch_bounds__(256) mean_u_kernel(const double* __restrict__ u, SolveCtl ctl, SlabGeo sg) {
   constexpr int NR = N / G;
-  __shared__ double scratch[32];
+  __shared__ double scratch[64];
   const int nlg = sg.nloc * G;
   const int b = blockIdx.x / nlg;
   const int rem = blockIdx.x - b * nlg;
