@@ -136,6 +136,11 @@ struct Ops {
   static size_t mid_smem(int r1) {
     return (size_t)mid_dsm_offset(N * (G * W + 1), G * W, r1) + (size_t)N * G * W * sizeof(double);
   }
+  // fused middle pass reads the precomputed diagonal from L2 (CHK_MID_DG=0: stage it in smem)
+  static bool mid_dg() {
+    static const bool on = !(getenv("CHK_MID_DG") && atoi(getenv("CHK_MID_DG")) == 0);
+    return on;
+  }
   static int maxblk() { return PLANE_BLOCKS > TILES ? PLANE_BLOCKS : TILES; }
   // single-GPU layout: all planes, one column chunk, periodic halo inside p
   static SlabGeo whole() { return SlabGeo{N, 0, 1, NR * H, 0, TILES, nullptr, nullptr}; }
@@ -213,6 +218,10 @@ struct Ops {
       if (SX) sm += (size_t)G * RA * NT * sizeof(double2);
       CHK_CUDA(allow_smem(mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT, SX>, sm));
       mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT, SX><<<grid, NT, sm, s>>>(S, pl, ctl, sg, it, B);
+    } else if (pl.D && mid_dg()) {
+      const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
+      CHK_CUDA(allow_smem(mid_column_fused_kernel<N, G, W, NBX, MODE, true>, sm));
+      mid_column_fused_kernel<N, G, W, NBX, MODE, true><<<grid, block, sm, s>>>(S, pl, ctl, sg, it, B);
     } else {
       const size_t sm = mid_smem(r1);
       CHK_CUDA(allow_smem(mid_column_fused_kernel<N, G, W, NBX, MODE>, sm));

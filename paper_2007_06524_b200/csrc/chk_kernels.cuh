@@ -124,6 +124,7 @@ template <int N>
 struct MidNT {
   static constexpr int value = (N == 512) ? CHK_NT512 : 256;
   static constexpr int minb = (N == 512) ? 1 : 2;
+  static constexpr int minb_dg = (N == 512) ? 1 : 3;  // diagonal read from L2: tile-only smem
 };
 template <int N>
 struct IlC {  // CTAs per cluster of the plane passes
@@ -1070,9 +1071,12 @@ __device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restri
 // memory, [last forward stage + residual update + scaling + Parseval + first
 // inverse stage] in registers, remaining inverse stages, inverse group combine
 // + store in registers: 12 shared-memory passes per element instead of 20.
-template <int N, int G, int W, int NB, int MODE>
-__global__ void __launch_bounds__(MidNT<N>::value, MidNT<N>::minb) mid_column_fused_kernel(double2* __restrict__ S, PlanDev pl,
-                                                               SolveCtl ctl, SlabGeo sg, int it, int B) {
+// DG: the diagonal tile is read from the plan's precomputed table (L2) in the
+// fused last stage instead of being staged in shared memory -- the tile alone
+// then fits 3 CTAs per SM at n = 256 (2 with the staged diagonal).
+template <int N, int G, int W, int NB, int MODE, bool DG = false>
+__global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidNT<N>::minb)
+    mid_column_fused_kernel(double2* __restrict__ S, PlanDev pl, SolveCtl ctl, SlabGeo sg, int it, int B) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
@@ -1130,13 +1134,24 @@ __global__ void __launch_bounds__(MidNT<N>::value, MidNT<N>::minb) mid_column_fu
     while (j0 < NB && !s_act[j0]) ++j0;
     prefetch(j0);
   }
-  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
+  __shared__ int s_dc;  // DG: slot of the zero frequency (k1 = k2 = 0) in this tile, or -1
+  const double* Dg = nullptr;
+  if constexpr (DG) {
+    mid_slots<N, G, W>(cg0, pl, s_k1, s_k2, s_wgt, s_tw);
+    if (threadIdx.x == 0) s_dc = -1;
+    __syncthreads();
+    if (MODE != MID_APPLY && threadIdx.x < GW && s_k1[threadIdx.x] == 0 && s_k2[threadIdx.x] == 0)
+      s_dc = threadIdx.x;
+    __syncthreads();
+    Dg = pl.D + (size_t)(cg0 / W) * N * GW;
+  } else {
+    mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
+  }
   const double scale = 2.0 / ((double)N * N * N);
   for (int j = 0; j < NB; ++j) {
     if (!s_act[j]) continue;
     const int b = b0 + j;
     // ---- load + group combine (registers) -> smem ----
-#pragma unroll 2
     for (int item = threadIdx.x; item < N * W; item += blockDim.x) {
       const int w = item % W, x0 = item / W;
       const size_t rbase = slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), 0) + (IL ? c0 * G : c0) + w;
@@ -1168,8 +1183,14 @@ __global__ void __launch_bounds__(MidNT<N>::value, MidNT<N>::minb) mid_column_fu
 #pragma unroll
       for (int e = 0; e < RL; ++e) {
         const int pos0 = blk * RL + e;
-        v[e] = mid_point<MODE>(v[e], Dsm[pos0 * GW + s], s_wgt[s], scale, s_alpha[j],
-                               Rt + (size_t)pos0 * GW + s, rr, rz);
+        double D;
+        if constexpr (DG) {
+          // mean projection of z (solver.py:153,179): the zero-frequency coefficient is 0
+          D = (pos0 == 0 && s == s_dc) ? 0.0 : __ldg(Dg + pos0 * GW + s);
+        } else {
+          D = Dsm[pos0 * GW + s];
+        }
+        v[e] = mid_point<MODE>(v[e], D, s_wgt[s], scale, s_alpha[j], Rt + (size_t)pos0 * GW + s, rr, rz);
       }
       dftR<RL, true>(v);
 #pragma unroll
