@@ -26,6 +26,9 @@
 #ifndef CHK_FUSED_PF  // L2 prefetch of the next realization in the fused middle pass
 #define CHK_FUSED_PF 0
 #endif
+#ifndef CHK_MARCH  // marching stencil in the plane passes (n = 64, 128)
+#define CHK_MARCH 1
+#endif
 #ifndef CHK_MID_RPF
 #define CHK_MID_RPF 1
 #endif
@@ -119,6 +122,7 @@ struct IlW {
 template <int N>
 struct PlaneNT {
   static constexpr int value = (N == 512) ? CHK_NT512 : 256;
+  static constexpr int minb = (N == 512) ? 1 : 3;  // <= 85 registers: 3 CTAs per SM (66.5 KB slabs)
 };
 template <int N>
 struct MidNT {
@@ -438,6 +442,37 @@ __device__ __forceinline__ void ldg4v(const double* p, double (&v)[4]) {
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
 }
 
+// Arithmetic of the all-inside quad: p rows (center, x0 -+ 1, x1 -+ 1), the x2
+// halo (pl, prr) and the eight cell values m.. (cells of x2s - 1) / z.. (cells
+// of x2s) for the (x0-1|x0, x1-1|x1) cell rows.
+__device__ __forceinline__ void stencil4_allin_q(double lam, const double (&pc)[4], const double (&xm)[4],
+                                                 const double (&xp)[4], const double (&ym)[4],
+                                                 const double (&yp)[4], double pl, double prr, double m00,
+                                                 double m01, double m10, double m11, double z00, double z01,
+                                                 double z10, double z11, double (&q)[4]) {
+  auto wsum = [lam](double a, double b, double c, double d) { return lam + (((a + b) + c) + d) * 0.25; };
+  // node 0: h-cells x2-1 -> m.., x2 -> z..
+  const double A0p = wsum(z11, m11, z10, m10), A0m = wsum(z01, m01, z00, m00);
+  const double A1p = wsum(z11, m11, z01, m01), A1m = wsum(z10, m10, z00, m00);
+  const double A2p = wsum(z11, z10, z01, z00), A2m = wsum(m11, m10, m01, m00);
+  // nodes 1..3: both h-cells in the quad's cell
+  const double B0p = wsum(z11, z11, z10, z10), B0m = wsum(z01, z01, z00, z00);
+  const double B1p = wsum(z11, z11, z01, z01), B1m = wsum(z10, z10, z00, z00);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double g0p = i ? B0p : A0p, g0m = i ? B0m : A0m;
+    const double g1p = i ? B1p : A1p, g1m = i ? B1m : A1m;
+    const double g2p = A2p, g2m = i ? A2p : A2m;
+    const double c = pc[i];
+    const double left = (i == 0) ? pl : pc[i - 1];
+    const double right = (i == 3) ? prr : pc[i + 1];
+    const double q0 = g0p * (c - xp[i]) + g0m * (c - xm[i]);
+    const double q1 = g1p * (c - yp[i]) + g1m * (c - ym[i]);
+    const double q2 = g2p * (c - right) + g2m * (c - left);
+    q[i] = (q0 + q1) + q2;
+  }
+}
+
 template <int N>
 __device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
                                                const double* __restrict__ beta, int x0, int x1,
@@ -474,27 +509,72 @@ __device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
   const double* b11 = beta + ((size_t)c00 * L + c10) * L;  // (x0,   x1)
   const double m00 = __ldg(b00 + cm), m01 = __ldg(b01 + cm), m10 = __ldg(b10 + cm), m11 = __ldg(b11 + cm);
   const double z00 = __ldg(b00 + cc), z01 = __ldg(b01 + cc), z10 = __ldg(b10 + cc), z11 = __ldg(b11 + cc);
-  const double lam = g.lam;
-  auto wsum = [lam](double a, double b, double c, double d) { return lam + (((a + b) + c) + d) * 0.25; };
-  // node 0: h-cells x2-1 -> m.., x2 -> z..
-  const double A0p = wsum(z11, m11, z10, m10), A0m = wsum(z01, m01, z00, m00);
-  const double A1p = wsum(z11, m11, z01, m01), A1m = wsum(z10, m10, z00, m00);
-  const double A2p = wsum(z11, z10, z01, z00), A2m = wsum(m11, m10, m01, m00);
-  // nodes 1..3: both h-cells in the quad's cell
-  const double B0p = wsum(z11, z11, z10, z10), B0m = wsum(z01, z01, z00, z00);
-  const double B1p = wsum(z11, z11, z01, z01), B1m = wsum(z10, z10, z00, z00);
+  stencil4_allin_q(g.lam, pc, xm, xp, ym, yp, pl, prr, m00, m01, m10, m11, z00, z01, z10, z11, q);
+}
+
+// Marching form of the all-inside stencil for the plane passes (n = 64, 128:
+// Q4 lanes cover one row, G <= 2): the lanes of a row group walk RPS
+// consecutive group rows t, x1 = gg + G t, so the x1 - 1 row of a step is the
+// x1 + 1 row of the previous one (G = 2; G = 1 also reuses the centre row):
+// 4 (3) row loads per step instead of 5.  The cell values of x2s - 1 come from
+// lane - 1 by shuffle (the quad is one aligned 4-node run inside a cell, n0 >= 4).
+// Same formulas as stencil4_allin; q goes to the smem row of t, <p, q> into acc.
+template <int N, int G, int NR>
+__device__ __forceinline__ void stencil_march(const Geo& g, const Planes& P3, const double* __restrict__ beta,
+                                              int x0, int gg, double* sm, int rowpitch, double& acc) {
+  constexpr int nm = N - 1;
+  constexpr int Q4 = N / 4;
+  static_assert(Q4 == 16 || Q4 == 32, "one row per 16/32 lanes");
+  static_assert(G == 1 || G == 2, "row reuse along x1 needs G <= 2");
+  const int nsub = blockDim.x / Q4;
+  const int RPS = NR / nsub;  // rows per lane group
+  const int sub = threadIdx.x / Q4, lane = threadIdx.x % Q4;
+  const int x2s = 4 * lane;
+  const int L = g.L, sh = g.sh;
+  const int c0m = ((x0 - 1) & nm) >> sh, c00 = x0 >> sh;
+  const int cc = x2s >> sh;
+  const int t0 = sub * RPS;
+  double ym[4], pc[4];
+  {
+    const int x1 = gg + G * t0;
+    ldg4v(P3.c + (long long)((x1 - 1) & nm) * N + x2s, ym);
+    if (G == 1) ldg4v(P3.c + (long long)x1 * N + x2s, pc);
+  }
+  for (int k = 0; k < RPS; ++k) {
+    const int t = t0 + k;
+    const int x1 = gg + G * t;
+    const long long row = (long long)x1 * N + x2s;
+    double xm[4], xp[4], yp[4];
+    if (G == 2) ldg4v(P3.c + row, pc);
+    ldg4v(P3.c + (long long)((x1 + 1) & nm) * N + x2s, yp);
+    ldg4v(P3.m + row, xm);
+    ldg4v(P3.p + row, xp);
+    const int c1m = ((x1 - 1) & nm) >> sh, c10 = x1 >> sh;
+    const double* b00 = beta + ((size_t)c0m * L + c1m) * L;
+    const double* b01 = beta + ((size_t)c0m * L + c10) * L;
+    const double* b10 = beta + ((size_t)c00 * L + c1m) * L;
+    const double* b11 = beta + ((size_t)c00 * L + c10) * L;
+    const double z00 = __ldg(b00 + cc), z01 = __ldg(b01 + cc), z10 = __ldg(b10 + cc), z11 = __ldg(b11 + cc);
+    const int src = (lane - 1) & (Q4 - 1);
+    const double m00 = __shfl_sync(0xffffffffu, z00, src, Q4), m01 = __shfl_sync(0xffffffffu, z01, src, Q4);
+    const double m10 = __shfl_sync(0xffffffffu, z10, src, Q4), m11 = __shfl_sync(0xffffffffu, z11, src, Q4);
+    const double pl = __shfl_sync(0xffffffffu, pc[3], src, Q4);
+    const double prr = __shfl_sync(0xffffffffu, pc[0], (lane + 1) & (Q4 - 1), Q4);
+    double q[4];
+    stencil4_allin_q(g.lam, pc, xm, xp, ym, yp, pl, prr, m00, m01, m10, m11, z00, z01, z10, z11, q);
+    double2* s2 = reinterpret_cast<double2*>(sm + t * rowpitch + x2s);
+    s2[0] = make_double2(q[0], q[1]);
+    s2[1] = make_double2(q[2], q[3]);
+    acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double g0p = i ? B0p : A0p, g0m = i ? B0m : A0m;
-    const double g1p = i ? B1p : A1p, g1m = i ? B1m : A1m;
-    const double g2p = A2p, g2m = i ? A2p : A2m;
-    const double c = pc[i];
-    const double left = (i == 0) ? pl : pc[i - 1];
-    const double right = (i == 3) ? prr : pc[i + 1];
-    const double q0 = g0p * (c - xp[i]) + g0m * (c - xm[i]);
-    const double q1 = g1p * (c - yp[i]) + g1m * (c - ym[i]);
-    const double q2 = g2p * (c - right) + g2m * (c - left);
-    q[i] = (q0 + q1) + q2;
+    for (int e = 0; e < 4; ++e) {
+      if (G == 1) {
+        ym[e] = pc[e];
+        pc[e] = yp[e];
+      } else {
+        ym[e] = yp[e];
+      }
+    }
   }
 }
 
@@ -732,14 +812,18 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
     P3.m = (x0l > 0) ? P3.c - nn : (sg.halo_lo ? sg.halo_lo + b * nn : pb + (size_t)(N - 1) * nn);
     P3.p = (x0l < sg.nloc - 1) ? P3.c + nn : (sg.halo_hi ? sg.halo_hi + b * nn : pb);
     double acc = 0.0;
-    for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
-      const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
-      double pc[4], q[4];
-      stencil_quad<N, ALLIN>(g, P3, bb, x0, gg + G * t, x2, pc, q);
-      double2* s2 = reinterpret_cast<double2*>(sm + t * 2 * HP + x2);
-      s2[0] = make_double2(q[0], q[1]);
-      s2[1] = make_double2(q[2], q[3]);
-      acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
+    if constexpr (ALLIN && CHK_MARCH && (Q4 == 16 || Q4 == 32) && G <= 2) {
+      stencil_march<N, G, NR>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
+    } else {
+      for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
+        const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
+        double pc[4], q[4];
+        stencil_quad<N, ALLIN>(g, P3, bb, x0, gg + G * t, x2, pc, q);
+        double2* s2 = reinterpret_cast<double2*>(sm + t * 2 * HP + x2);
+        s2[0] = make_double2(q[0], q[1]);
+        s2[1] = make_double2(q[2], q[3]);
+        acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
+      }
     }
     double t0, t1;
     if (reduce2_last(acc, 0.0, ctl.part + (size_t)b * 2 * ctl.maxblk, &st->cnt, rem, nlg,

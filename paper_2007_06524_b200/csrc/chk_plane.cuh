@@ -15,7 +15,7 @@ namespace chk {
 // plane-pass kernels
 // --------------------------------------------------------------------------
 template <int N, int G, int MODE, bool ALLIN>
-__global__ void __launch_bounds__(PlaneNT<N>::value) fwd_plane_kernel(Geo g, const double* __restrict__ beta,
+__global__ void __launch_bounds__(PlaneNT<N>::value, PlaneNT<N>::minb) fwd_plane_kernel(Geo g, const double* __restrict__ beta,
                                                         const double* __restrict__ src, double* __restrict__ u,
                                                         double2* __restrict__ S, PlanDev pl,
                                                         SolveCtl ctl, SlabGeo sg, int B, int it) {
@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(PlaneNT<N>::value) fwd_plane_kernel(Geo g, con
 }
 
 template <int N, int G, int MODE>
-__global__ void __launch_bounds__(PlaneNT<N>::value) inv_plane_kernel(const double2* __restrict__ S,
+__global__ void __launch_bounds__(PlaneNT<N>::value, PlaneNT<N>::minb) inv_plane_kernel(const double2* __restrict__ S,
                                                         double* __restrict__ out, double* __restrict__ u,
                                                         PlanDev pl, SolveCtl ctl, SlabGeo sg, int B, int it) {
   inv_plane_body<N, G, MODE>(S, out, u, pl, ctl, sg, B, it, blockIdx.x);
