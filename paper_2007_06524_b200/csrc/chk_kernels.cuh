@@ -29,6 +29,9 @@
 #ifndef CHK_MARCH  // marching stencil in the plane passes (n = 64, 128)
 #define CHK_MARCH 1
 #endif
+#ifndef CHK_FWD_PF  // L2 prefetch of the CTA's own p rows at the start of the forward pass
+#define CHK_FWD_PF 1
+#endif
 #ifndef CHK_MID_RPF
 #define CHK_MID_RPF 1
 #endif
@@ -811,6 +814,8 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
     P3.c = pb + (size_t)x0l * nn;
     P3.m = (x0l > 0) ? P3.c - nn : (sg.halo_lo ? sg.halo_lo + b * nn : pb + (size_t)(N - 1) * nn);
     P3.p = (x0l < sg.nloc - 1) ? P3.c + nn : (sg.halo_hi ? sg.halo_hi + b * nn : pb);
+    if (CHK_FWD_PF && threadIdx.x < NR)  // this CTA's rows of p: start the DRAM reads now
+      bulk_prefetch_l2(P3.c + (size_t)(gg + G * threadIdx.x) * N, N * sizeof(double));
     double acc = 0.0;
     if constexpr (ALLIN && CHK_MARCH && (Q4 == 16 || Q4 == 32) && G <= 2) {
       stencil_march<N, G, NR>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
