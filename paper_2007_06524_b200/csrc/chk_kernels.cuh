@@ -515,6 +515,27 @@ __device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
   stencil4_allin_q(g.lam, pc, xm, xp, ym, yp, pl, prr, m00, m01, m10, m11, z00, z01, z10, z11, q);
 }
 
+// Quad (4 consecutive doubles of a smem row, x2s % 4 == 0) as two 16-byte
+// accesses in a swizzled order: quads 4i..4i+3 start with their low half, quads
+// 4i+4..4i+7 with their high half, so a warp's 32 consecutive quads (32-byte
+// lane stride) hit every bank exactly 4 times per instruction (the plain order
+// is a 2-way bank conflict).
+__device__ __forceinline__ void st_quad_smem(double* rowp, int x2s, const double (&q)[4]) {
+  double2* s2 = reinterpret_cast<double2*>(rowp + x2s);
+  const int h = (x2s >> 4) & 1;
+  const double2 lo = make_double2(q[0], q[1]), hi = make_double2(q[2], q[3]);
+  s2[h] = h ? hi : lo;
+  s2[h ^ 1] = h ? lo : hi;
+}
+__device__ __forceinline__ void ld_quad_smem(const double* rowp, int x2s, double (&q)[4]) {
+  const double2* s2 = reinterpret_cast<const double2*>(rowp + x2s);
+  const int h = (x2s >> 4) & 1;
+  const double2 a = s2[h];
+  const double2 b = s2[h ^ 1];
+  const double2 lo = h ? b : a, hi = h ? a : b;
+  q[0] = lo.x; q[1] = lo.y; q[2] = hi.x; q[3] = hi.y;
+}
+
 // Marching form of the all-inside stencil for the plane passes (n = 64, 128:
 // Q4 lanes cover one row, G <= 2): the lanes of a row group walk RPS
 // consecutive group rows t, x1 = gg + G t, so the x1 - 1 row of a step is the
@@ -565,9 +586,7 @@ __device__ __forceinline__ void stencil_march(const Geo& g, const Planes& P3, co
     const double prr = __shfl_sync(0xffffffffu, pc[0], (lane + 1) & (Q4 - 1), Q4);
     double q[4];
     stencil4_allin_q(g.lam, pc, xm, xp, ym, yp, pl, prr, m00, m01, m10, m11, z00, z01, z10, z11, q);
-    double2* s2 = reinterpret_cast<double2*>(sm + t * rowpitch + x2s);
-    s2[0] = make_double2(q[0], q[1]);
-    s2[1] = make_double2(q[2], q[3]);
+    st_quad_smem(sm + t * rowpitch, x2s, q);
     acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -824,9 +843,7 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
         const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
         double pc[4], q[4];
         stencil_quad<N, ALLIN>(g, P3, bb, x0, gg + G * t, x2, pc, q);
-        double2* s2 = reinterpret_cast<double2*>(sm + t * 2 * HP + x2);
-        s2[0] = make_double2(q[0], q[1]);
-        s2[1] = make_double2(q[2], q[3]);
+        st_quad_smem(sm + t * 2 * HP, x2, q);
         acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
       }
     }
@@ -1692,9 +1709,7 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     const size_t idx = b * nb + ((size_t)x0 * N + gg + G * t) * N + x2;
     double z[4] = {0.0, 0.0, 0.0, 0.0};
     if (do_p) {
-      const double2 za = *reinterpret_cast<const double2*>(sm + t * 2 * HP + x2);
-      const double2 zb = *reinterpret_cast<const double2*>(sm + t * 2 * HP + x2 + 2);
-      z[0] = za.x; z[1] = za.y; z[2] = zb.x; z[3] = zb.y;
+      ld_quad_smem(sm + t * 2 * HP, x2, z);
     }
     if (MODE == INV_APPLY || MODE == INV_INIT) {
       stv4(out + idx, z);
