@@ -197,3 +197,31 @@ def test_paired_schedule_matches_oracle(monkeypatch, kind):
         monkeypatch.setenv("CHK_PAIR", "2")
         assert np.array_equal(res.iterations, ref.iterations)
         assert torch.equal(res.u, ref.u)  # the schedule does not change any realization's bits
+
+
+@pytest.mark.parametrize("n0,L,kind", [(4, 16, "lkr"), (4, 16, "fourier"), (4, 64, "lkr")])
+def test_precomputed_diagonal_tiles_bitwise(monkeypatch, n0, L, kind):
+    """Plans evaluate every middle-pass diagonal tile once (dtile_kernel) and the
+    middle passes stream them; CHK_NO_DTILE=1 evaluates the same contraction per
+    CTA.  Same formula, same order: identical bits (n = 64: register middle pass,
+    n = 256: fused middle pass reading the tiles from L2)."""
+    from paper_2007_06524_b200.lowrank import _device_apply, _plan_for
+    from paper_2007_06524_b200.solver import Preconditioner
+
+    cfg = chk.LatticeConfig(d=3, L=L, n0=n0, alpha="1/2", lam=0.1)
+    B = 3 if L <= 16 else 1
+    beta = np.stack([chk.sample_realization(cfg, chk.derive_seed(0, m)).beta_cells.ravel() for m in range(B)])
+    A = chk.StiffnessBatch(cfg, beta)
+    F = chk.corrector_rhs_batched(A, 1)
+    opts = chk.SolveOptions(tol=1e-8, preconditioner=kind, eps_rank=1e-8)
+    res = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("CHK_NO_DTILE", flag)
+        plan = _plan_for(3, cfg.n, kind, 1e-8 if kind == "lkr" else 0.0, 0.0)
+        P = Preconditioner(kind, lambda x, p=plan: _device_apply(p, x), plan)
+        r = chk.pcg_solve_batched(A, F, opts, P)
+        assert np.all(r.status == 0)
+        res[flag] = (r.iterations.copy(), r.u.clone(), P.apply(F))
+    assert np.array_equal(res["0"][0], res["1"][0])
+    assert torch.equal(res["0"][1], res["1"][1])
+    assert torch.equal(res["0"][2], res["1"][2])
