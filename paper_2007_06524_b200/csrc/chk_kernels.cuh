@@ -32,6 +32,9 @@
 #ifndef CHK_FWD_PF  // L2 prefetch of the CTA's own p rows at the start of the forward pass
 #define CHK_FWD_PF 1
 #endif
+#ifndef CHK_INV_PF  // L2 prefetch of the p / u rows at the start of the inverse pass (n <= 128;
+#define CHK_INV_PF 1    // at n >= 256 the prefetched rows are evicted before use: +38 % DRAM reads)
+#endif
 #ifndef CHK_MID_RPF
 #define CHK_MID_RPF 1
 #endif
@@ -1681,7 +1684,7 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
                  (uint32_t)(sg.ncols * sizeof(double2)), &bar);
     }
   }
-  if (MODE == INV_ITER && threadIdx.x < NR) {
+  if (MODE == INV_ITER && CHK_INV_PF && N <= 128 && threadIdx.x < NR) {
     // p and u rows of this slab are read after the transforms: warm L2 now
     const size_t ro = b * nb + ((size_t)x0 * N + gg + G * threadIdx.x) * N;
     bulk_prefetch_l2(out + ro, N * sizeof(double));
