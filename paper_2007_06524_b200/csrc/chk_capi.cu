@@ -111,8 +111,14 @@ struct Cfg;
 template <> struct Cfg<8>   { static constexpr int G = 1,  W = 8,  NB = 4, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<16>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4, REG = 1, RA = 8, P = 1; };
-template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = 16, REG = 1, RA = 8, P = 1; };
-template <> struct Cfg<128> { static constexpr int G = 2,  W = CHK_W128, NB = 16, REG = 1, RA = 8, P = 1; };
+#ifndef CHK_NB64
+#define CHK_NB64 4
+#endif
+#ifndef CHK_NB128
+#define CHK_NB128 16
+#endif
+template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = CHK_NB64, REG = 1, RA = 8, P = 1; };
+template <> struct Cfg<128> { static constexpr int G = 2,  W = CHK_W128, NB = CHK_NB128, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 16, REG = 0, RA = 1, P = 1; };
 template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2, REG = 0, RA = 1, P = 1; };
 
@@ -327,16 +333,16 @@ struct Ops {
   }
 
 // Realizations in the first half of a paired solve (0: unpaired).  Pairing pays
-// only while each half alone still runs the middle pass with the diagonal tile
-// amortised over NB realizations on >= 2 CTAs per SM (measured: config 3 +3 %,
-// config 2 -25 % when its 32-realization halves lose the NB grouping, config 4
-// neutral).  CHK_PAIR=0 disables it, CHK_PAIR=2 forces it for any B >= 2 (tests).
+// at n = 128 only, while each half alone still fills >= 2 CTAs per SM in the
+// middle pass (measured: config 3 +1.4 %; config 2 (n = 64) -19 %, config 4
+// (n = 256) -1.5 %).  CHK_PAIR=0 disables it, CHK_PAIR=2 forces it for any
+// B >= 2 (tests).
 template <class O>
 int pair_split(int B) {
   const char* e = getenv("CHK_PAIR");
   const int env = e ? atoi(e) : 1;
   if (env == 2 && B >= 2) return B / 2;
-  if (!env || !O::REG || B < 2 * O::NB) return 0;
+  if (!env || !O::REG || O::NN != 128 || B < 2 * O::NB) return 0;
   const int Ba = (B / 2) / O::NB * O::NB;
   const int Bb = B - Ba;
   const long long ctas = (long long)(Ba / O::NB) * O::TILES;
