@@ -119,7 +119,10 @@ template <> struct Cfg<32>  { static constexpr int G = 1,  W = 16, NB = 4, REG =
 #endif
 template <> struct Cfg<64>  { static constexpr int G = 1,  W = 16, NB = CHK_NB64, REG = 1, RA = 8, P = 1; };
 template <> struct Cfg<128> { static constexpr int G = 2,  W = CHK_W128, NB = CHK_NB128, REG = 1, RA = 8, P = 1; };
-template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = 16, REG = 0, RA = 1, P = 1; };
+#ifndef CHK_NB256
+#define CHK_NB256 8
+#endif
+template <> struct Cfg<256> { static constexpr int G = 8,  W = 2,  NB = CHK_NB256, REG = 0, RA = 1, P = 1; };
 template <> struct Cfg<512> { static constexpr int G = 16, W = 1,  NB = 2, REG = 0, RA = 1, P = 1; };
 
 // every h-cell inside its sub-cell (alpha = 1/2): stencil fast path
