@@ -6,6 +6,7 @@ records its outputs for the hot path.  The fixtures pin both the CPU oracle
 
     python tests/golden/make_golden.py small            # -> tests/golden/small.npz
     python tests/golden/make_golden.py config 3 0 16    # -> tests/golden/config3_0_16.json
+    python tests/golden/make_golden.py formats          # -> tests/golden/formats.json
 
 Large arrays are never committed: for configs 2-5 we keep iteration counts,
 the full residual history, ||u||, <u, f>, <u, w> for a seeded Gaussian w and
@@ -251,8 +252,42 @@ def configs(cfg_id: int, start: int, count: int):
                        "numpy": np.__version__, "records": recs}, fh, indent=1)
 
 
+def formats():
+    """Wire formats around the path: realization JSON
+    (lattice.py:229-250) for every contrast kind / offset, and the CSV cell
+    formatting of cli.py:264-267,281-287 applied to a pcg_solve trace."""
+    cases = [
+        dict(d=3, L=4, n0=4, alpha="1/2", lam=0.1),
+        dict(d=3, L=3, n0=8, alpha="1/4", lam=0.4, subcell_offset=1),
+        dict(d=3, L=4, n0=4, alpha="1/2", lam=0.2, contrast=ch.ContrastModel.two_value(0.3, 0.7)),
+        dict(d=3, L=5, n0=4, alpha="1/4", lam=0.4, contrast=ch.ContrastModel.layered([0.1, 0.5, 0.2])),
+        dict(d=2, L=6, n0=4, alpha="1/2", lam=0.5, coverage_prob=0.3),
+    ]
+    recs = []
+    for i, kw in enumerate(cases):
+        cfg = ch.LatticeConfig(**kw)
+        r = ch.sample_realization(cfg, ch.derive_seed(3, i))
+        recs.append({"config_dict": cfg.to_dict(), "seed": int(r.seed), "json": r.to_json()})
+    cfg = ch.LatticeConfig(d=3, L=4, n0=4, alpha="1/2", lam=0.1)
+    r = ch.sample_realization(cfg, ch.derive_seed(0, 0))
+    A = ch.assemble_stiffness(r)
+    f = (1.0 / cfg.n) ** (2 - 3) * ch.corrector_rhs(r, 1)
+    u, rep = ch.pcg_solve(A, f, ch.SolveOptions(tol=1e-8, preconditioner="lkr"))
+    from checkerhom.cli import _fmt
+    rows = [",".join(_fmt(v) for v in row) for row in enumerate(rep.residuals, start=1)]
+    doc = {"generator": "tests/golden/make_golden.py formats (reference checkerhom)",
+           "realizations": recs,
+           "trace": {"config": cfg.to_dict(), "seed": int(r.seed), "iterations": rep.iterations,
+                     "residuals": [float(x) for x in rep.residuals], "csv_rows": rows,
+                     "preconditioner": rep.preconditioner}}
+    with open(os.path.join(HERE, "formats.json"), "w") as fh:
+        json.dump(doc, fh, indent=1)
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "small":
         small()
+    elif sys.argv[1] == "formats":
+        formats()
     else:
         configs(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]))
