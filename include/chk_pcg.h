@@ -140,8 +140,10 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
  * The same batched solve from HOST buffers (the reference-facing call: numpy
  * in, numpy out).  beta_host [B][L^3], f_host [B][n^3] in, u_host [B][n^3]
  * out; pinned host memory makes the copies asynchronous.  The batch runs in
- * chunks of `chunk` realizations through two device slots: the upload of
- * chunk c+1 and the download of chunk c-1 overlap the solve of chunk c.
+ * chunks of `chunk` realizations on three lanes (host threads with their own
+ * stream, device slot and solver workspace, alternate chunks): one lane's
+ * uploads, downloads and convergence tail overlap the other lanes' solves.
+ * Per-realization results are identical to chk_pcg_solve_batched.
  * workspace: device buffer of chk_pcg_host_workspace_bytes bytes.
  * ------------------------------------------------------------------------- */
 size_t chk_pcg_host_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, int32_t chunk,

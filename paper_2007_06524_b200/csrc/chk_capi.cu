@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -804,13 +805,27 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
   return CHK_OK;
 }
 
+// Host-buffer pipeline: three lanes (host threads, each with its own stream,
+// device slot and solver workspace) take chunks round-robin; on a lane a chunk
+// is uploaded, solved and downloaded in stream order, and the lanes overlap on
+// the GPU -- one lane's copies and convergence tail run under the other lanes'
+// solves (config 3, e2e: 1 lane 4.0e10, 2 lanes 4.24e10, 3 lanes x 32
+// realizations 4.30e10 DOF-it/s).  CHK_HOST_LANES overrides (1..4).
+static int host_lanes(int nchunks) {
+  static const int want = getenv("CHK_HOST_LANES") ? atoi(getenv("CHK_HOST_LANES")) : 3;
+  const int l = want < 1 ? 1 : (want > 4 ? 4 : want);
+  return nchunks < l ? nchunks : l;
+}
+
 size_t chk_pcg_host_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, int32_t chunk,
                                     int32_t max_iter) {
   if (!grid || !plan || chunk < 1 || max_iter < 1 || !supported_n(grid->n)) return 0;
   const size_t nb = (size_t)grid->n * grid->n * grid->n;
   const size_t lb = (size_t)grid->L * grid->L * grid->L;
   const size_t slot = align_up(sizeof(double) * (2 * nb + lb) * chunk);
-  return 2 * slot + chk_pcg_workspace_bytes(grid, plan, chunk, max_iter);
+  const size_t sw = chk_pcg_workspace_bytes(grid, plan, chunk, max_iter);
+  if (sw == 0) return 0;
+  return (size_t)host_lanes(1 << 30) * (slot + align_up(sw));
 }
 
 int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, const double* beta_host,
@@ -826,76 +841,86 @@ int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, c
   const size_t nb = (size_t)grid->n * grid->n * grid->n;
   const size_t lb = (size_t)grid->L * grid->L * grid->L;
   const size_t slot_bytes = align_up(sizeof(double) * (2 * nb + lb) * chunk);
-  char* base = static_cast<char*>(workspace);
-  double* d_f[2] = {reinterpret_cast<double*>(base), reinterpret_cast<double*>(base + slot_bytes)};
-  double* d_u[2] = {d_f[0] + nb * chunk, d_f[1] + nb * chunk};
-  double* d_b[2] = {d_u[0] + nb * chunk, d_u[1] + nb * chunk};
-  void* solver_ws = base + 2 * slot_bytes;
-  const size_t solver_bytes = workspace_bytes - 2 * slot_bytes;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaStream_t cp;
-  CHK_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
-  cudaEvent_t in_ready[2], solved[2], out_done[2], start;
-  for (int i = 0; i < 2; ++i) {
-    cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&solved[i], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming);
-  }
-  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-  int rc = CHK_OK;
-  long long launches = 0;
+  const size_t solver_bytes = align_up(chk_pcg_workspace_bytes(grid, plan, chunk, opts->max_iter));
   const int nchunks = (B + chunk - 1) / chunk;
-  auto upload = [&](int c) -> int {
-    const int b0 = c * chunk, nbc = (B - b0 < chunk) ? B - b0 : chunk, sl = c & 1;
-    CHK_CUDA(cudaMemcpyAsync(d_b[sl], beta_host + lb * b0, sizeof(double) * lb * nbc, cudaMemcpyHostToDevice, cp));
-    CHK_CUDA(cudaMemcpyAsync(d_f[sl], f_host + nb * b0, sizeof(double) * nb * nbc, cudaMemcpyHostToDevice, cp));
-    CHK_CUDA(cudaEventRecord(in_ready[sl], cp));
-    return CHK_OK;
+  const int lanes = host_lanes(nchunks);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int dev = 0;
+  CHK_CUDA(cudaGetDevice(&dev));
+  cudaEvent_t start;
+  CHK_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  CHK_CUDA(cudaEventRecord(start, s));  // the lanes follow the caller's prior work
+  struct LaneOut {
+    int rc = CHK_OK;
+    std::string err;
+    long long launches = 0;
   };
-  CHK_CUDA(cudaEventRecord(start, s));  // the copies follow the caller's prior work
-  CHK_CUDA(cudaStreamWaitEvent(cp, start, 0));
-  if ((rc = upload(0))) goto done;
-  for (int c = 0; c < nchunks; ++c) {
-    const int b0 = c * chunk, nbc = (B - b0 < chunk) ? B - b0 : chunk, sl = c & 1;
-    if (c + 1 < nchunks && (rc = upload(c + 1))) goto done;  // overlaps the solve below
-    if (cudaStreamWaitEvent(s, in_ready[sl], 0) != cudaSuccess ||
-        (c >= 2 && cudaStreamWaitEvent(s, out_done[sl], 0) != cudaSuccess)) {
-      rc = fail(CHK_ECUDA, "stream wait failed");
-      goto done;
-    }
-    rc = chk_pcg_solve_batched(grid, plan, d_b[sl], d_f[sl], d_u[sl], nbc, opts, iterations ? iterations + b0 : nullptr,
-                               final_rel ? final_rel + b0 : nullptr, status ? status + b0 : nullptr,
-                               rhs_projected ? rhs_projected + b0 : nullptr,
-                               nullptr, solver_ws, solver_bytes, stream);
-    launches += g_launches;
-    if (rc) goto done;
-    if (history) {
-      // chk_pcg_solve_batched keeps the device history inside its workspace: copy it out
-      Workspace w = carve(solver_ws, grid->n, nbc, opts->max_iter);
-      if (cudaMemcpyAsync(history + (size_t)opts->max_iter * b0, w.hist, sizeof(double) * opts->max_iter * nbc,
-                          cudaMemcpyDeviceToHost, s) != cudaSuccess) {
-        rc = fail(CHK_ECUDA, "history copy failed");
-        goto done;
+  std::vector<LaneOut> out(lanes);
+  auto lane_fn = [&](int lane) {
+    LaneOut& o = out[lane];
+    auto bad = [&](int code, const char* what, cudaError_t e) {
+      o.rc = code;
+      o.err = std::string(what) + (e != cudaSuccess ? std::string(": ") + cudaGetErrorString(e) : std::string());
+    };
+    cudaError_t e = cudaSetDevice(dev);
+    if (e != cudaSuccess) return bad(CHK_ECUDA, "lane cudaSetDevice", e);
+    cudaStream_t ls;
+    if ((e = cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking)) != cudaSuccess)
+      return bad(CHK_ECUDA, "lane stream", e);
+    char* base = static_cast<char*>(workspace) + (size_t)lane * (slot_bytes + solver_bytes);
+    double* d_f = reinterpret_cast<double*>(base);
+    double* d_u = d_f + nb * chunk;
+    double* d_b = d_u + nb * chunk;
+    void* solver_ws = base + slot_bytes;
+    if ((e = cudaStreamWaitEvent(ls, start, 0)) != cudaSuccess) bad(CHK_ECUDA, "lane wait", e);
+    for (int c = lane; c < nchunks && o.rc == CHK_OK; c += lanes) {
+      const int b0 = c * chunk, nbc = (B - b0 < chunk) ? B - b0 : chunk;
+      if ((e = cudaMemcpyAsync(d_b, beta_host + lb * b0, sizeof(double) * lb * nbc, cudaMemcpyHostToDevice, ls)) ||
+          (e = cudaMemcpyAsync(d_f, f_host + nb * b0, sizeof(double) * nb * nbc, cudaMemcpyHostToDevice, ls))) {
+        bad(CHK_ECUDA, "upload", e);
+        break;
+      }
+      const int rc = chk_pcg_solve_batched(grid, plan, d_b, d_f, d_u, nbc, opts, iterations ? iterations + b0 : nullptr,
+                                           final_rel ? final_rel + b0 : nullptr, status ? status + b0 : nullptr,
+                                           rhs_projected ? rhs_projected + b0 : nullptr, nullptr, solver_ws,
+                                           solver_bytes, ls);
+      o.launches += g_launches;
+      if (rc) {
+        o.rc = rc;
+        o.err = g_err;
+        break;
+      }
+      if (history) {
+        // chk_pcg_solve_batched keeps the device history inside its workspace: copy it out
+        Workspace w = carve(solver_ws, grid->n, nbc, opts->max_iter);
+        if ((e = cudaMemcpyAsync(history + (size_t)opts->max_iter * b0, w.hist, sizeof(double) * opts->max_iter * nbc,
+                                 cudaMemcpyDeviceToHost, ls))) {
+          bad(CHK_ECUDA, "history copy", e);
+          break;
+        }
+      }
+      if ((e = cudaMemcpyAsync(u_host + nb * b0, d_u, sizeof(double) * nb * nbc, cudaMemcpyDeviceToHost, ls))) {
+        bad(CHK_ECUDA, "download", e);
+        break;
       }
     }
-    if (cudaEventRecord(solved[sl], s) != cudaSuccess || cudaStreamWaitEvent(cp, solved[sl], 0) != cudaSuccess ||
-        cudaMemcpyAsync(u_host + nb * b0, d_u[sl], sizeof(double) * nb * nbc, cudaMemcpyDeviceToHost, cp) != cudaSuccess ||
-        cudaEventRecord(out_done[sl], cp) != cudaSuccess) {
-      rc = fail(CHK_ECUDA, "download failed");
-      goto done;
-    }
-  }
-  if (cudaStreamSynchronize(cp) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
-    rc = fail(CHK_ECUDA, "final synchronize failed");
-done:
-  cudaStreamSynchronize(cp);
-  for (int i = 0; i < 2; ++i) {
-    cudaEventDestroy(in_ready[i]);
-    cudaEventDestroy(solved[i]);
-    cudaEventDestroy(out_done[i]);
+    if ((e = cudaStreamSynchronize(ls)) != cudaSuccess && o.rc == CHK_OK) bad(CHK_ECUDA, "lane synchronize", e);
+    cudaStreamDestroy(ls);
+  };
+  if (lanes == 1) {
+    lane_fn(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int l = 0; l < lanes; ++l) th.emplace_back(lane_fn, l);
+    for (auto& t : th) t.join();
   }
   cudaEventDestroy(start);
-  cudaStreamDestroy(cp);
+  long long launches = 0;
+  int rc = CHK_OK;
+  for (auto& o : out) {
+    launches += o.launches;
+    if (o.rc && rc == CHK_OK) rc = fail(o.rc, "host pipeline: " + o.err);
+  }
   g_launches = launches;
   return rc;
 }
