@@ -285,7 +285,7 @@ struct Ops {
     if constexpr (IlC<N>::value > 1) return fail(CHK_EUNSUPPORTED, "paired plane pass with clustered plane CTAs");
     const size_t sm = plane_smem();
     const SlabGeo sg = whole();
-    dim3 grid(fa.blocks + ia.blocks), block(256);
+    dim3 grid(fa.blocks + ia.blocks), block(PlaneNT<N>::value);
     ProfScope ps(4, s);
     if (allin(fa.g)) {
       CHK_CUDA(allow_smem(pair_plane_kernel<N, G, true>, sm));

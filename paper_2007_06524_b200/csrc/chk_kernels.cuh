@@ -125,10 +125,14 @@ struct IlW {
 // (n = 256: 512-thread CTAs measured slower -- 64 registers spill -- for both.)
 // The fused middle pass states its 2 CTAs per SM at n <= 256 (<= 128 registers):
 // an explicit minimum of 1 lets nvcc take 164 registers and halves occupancy.
+#ifndef CHK_NT128
+#define CHK_NT128 256
+#endif
 template <int N>
 struct PlaneNT {
-  static constexpr int value = (N == 512) ? CHK_NT512 : 256;
-  static constexpr int minb = (N == 512) ? 1 : 3;  // <= 85 registers: 3 CTAs per SM (66.5 KB slabs)
+  static constexpr int value = (N == 512) ? CHK_NT512 : ((N == 128) ? CHK_NT128 : 256);
+  // 256 threads: <= 80 registers, 3 CTAs per SM (66.5 KB slabs); 512 threads at n = 128: 2 CTAs
+  static constexpr int minb = (N == 512) ? 1 : (value == 512 ? 2 : 3);
 };
 template <int N>
 struct MidNT {

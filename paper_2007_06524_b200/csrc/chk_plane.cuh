@@ -52,7 +52,7 @@ struct InvArgs {
 };
 
 template <int N, int G, bool ALLIN>
-__global__ void __launch_bounds__(256, 3) pair_plane_kernel(FwdArgs fa, InvArgs ia, PlanDev pl, SlabGeo sg) {
+__global__ void __launch_bounds__(PlaneNT<N>::value, PlaneNT<N>::minb) pair_plane_kernel(FwdArgs fa, InvArgs ia, PlanDev pl, SlabGeo sg) {
   const int m = fa.blocks < ia.blocks ? fa.blocks : ia.blocks;
   const int bx = blockIdx.x;
   bool fwd;
