@@ -23,9 +23,6 @@
 #include "chk_fft.cuh"
 #include "chk_tma.cuh"
 
-#ifndef CHK_FUSED_PF  // L2 prefetch of the next realization in the fused middle pass
-#define CHK_FUSED_PF 0
-#endif
 #ifndef CHK_MARCH  // marching stencil in the plane passes (n = 64, 128)
 #define CHK_MARCH 1
 #endif
@@ -1230,23 +1227,6 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
   }
   __syncthreads();
   if (scratch[0] == 0.0) return;
-  // Pull realization jj's tile into L2 while the one before it is transformed:
-  // the N spectrum rows (G*W*16 contiguous bytes each with the interleaved
-  // layout) and the contiguous residual tile.
-  auto prefetch = [&](int jj) {
-    if (!IL || !CHK_FUSED_PF || jj >= NB || !s_act[jj]) return;
-    const int bb = b0 + jj;
-    for (int x0 = threadIdx.x; x0 < N; x0 += blockDim.x)
-      bulk_prefetch_l2(S + slab_row(sg, B, G, x0 >> nsh, bb, x0 & (sg.nloc - 1), 0) + c0 * G,
-                       (uint32_t)(GW * sizeof(double2)));
-    if (MODE == MID_ITER && threadIdx.x == 0)
-      bulk_prefetch_l2(ctl.Rh + ((size_t)bb * TILES + tile) * N * GW, (uint32_t)(N * GW * sizeof(double2)));
-  };
-  {
-    int j0 = 0;
-    while (j0 < NB && !s_act[j0]) ++j0;
-    prefetch(j0);
-  }
   __shared__ int s_dc;  // DG: slot of the zero frequency (k1 = k2 = 0) in this tile, or -1
   const double* Dg = nullptr;
   if constexpr (DG) {
@@ -1276,11 +1256,6 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
       reg_fft<G, false>(v, pl.tw, N);
 #pragma unroll
       for (int g = 0; g < G; ++g) buf[x0 * RS + g * W + w] = v[g];
-    }
-    {
-      int jn = j + 1;
-      while (jn < NB && !s_act[jn]) ++jn;
-      prefetch(jn);
     }
     __syncthreads();
     FftRecButLast<N, N, false, GW>::run(buf, X0Addr{RS}, pl.tw, 1);
