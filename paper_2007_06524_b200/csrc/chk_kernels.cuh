@@ -1321,7 +1321,12 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
 // Shared memory is touched twice per element per direction (one exchange each
 // way).  P realizations are in flight per CTA; NB share one diagonal tile.
 
-template <int N, int G, int W, int RA, int NB, int P, int MODE, int NT, bool STG = false>
+// RSG (with STG, a precomputed plan diagonal and one phase-B item per thread):
+// the residual tile of the next realization arrives in shared memory by one
+// bulk copy (TMA) issued after the current realization's phase B, and the
+// thread's 16 diagonal values stay in registers for all NB realizations (no
+// shared diagonal tile) -- phase B then has no global-load latency.
+template <int N, int G, int W, int RA, int NB, int P, int MODE, int NT, bool STG = false, bool RSG = false>
 __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kernel(double2* __restrict__ S, PlanDev pl,
                                                                       SolveCtl ctl, SlabGeo sg, int it, int B) {
   constexpr int NR = N / G;
@@ -1370,7 +1375,20 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
   // STG: the phase-A tile of the next realization streams into a per-thread
   // staging area (cp.async) while the current one is transformed
   static_assert(!STG || (P == 1 && ITEMS_A == NT), "staging needs one phase-A item per thread");
-  double2* stg = reinterpret_cast<double2*>(reinterpret_cast<char*>(Dsm) + ((N * GW * 8 + 15) & ~15));
+  static_assert(!RSG || (STG && ITEMS_B == NT), "staged residual needs the staged variant, one phase-B item per thread");
+  // RSG layout: [buf N x RS][residual tile N x GW][phase-A staging]; otherwise [buf][Dsm][staging]
+  double2* rstg = reinterpret_cast<double2*>(reinterpret_cast<char*>(buf) + ((P * N * RS * 16 + 127) & ~127));
+  double2* stg = RSG ? rstg + N * GW
+                     : reinterpret_cast<double2*>(reinterpret_cast<char*>(Dsm) + ((N * GW * 8 + 15) & ~15));
+  __shared__ alignas(8) uint64_t rbar;
+  uint32_t rphase = 0;
+  auto issue_r = [&](int cc) {  // RSG: bulk copy of realization cc's residual tile
+    if (RSG && MODE == MID_ITER && cc < NB && s_act[cc] && threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)(N * GW * sizeof(double2));
+      mbar_arrive_expect_tx(&rbar, bytes);
+      bulk_g2s(rstg, ctl.Rh + ((size_t)(b0 + cc) * TILES + tile) * N * GW, bytes, &rbar);
+    }
+  };
   auto stage = [&](int cc) {
     if constexpr (STG) {
       if (sg.P == 1 && s_act[cc]) {
@@ -1388,16 +1406,39 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
   // the residual tile of a realization (N x GW, contiguous) is read in phase B:
   // pull it into L2 one realization ahead (the first one under the prologue)
   auto prefetch_r = [&](int cc) {
-    if (MODE == MID_ITER && CHK_MID_RPF && threadIdx.x == 0 && cc < NB / P) {
+    if (!RSG && MODE == MID_ITER && CHK_MID_RPF && threadIdx.x == 0 && cc < NB / P) {
       for (int pr = 0; pr < P; ++pr)
         if (s_act[cc * P + pr])
           bulk_prefetch_l2(ctl.Rh + ((size_t)(b0 + cc * P + pr) * TILES + tile) * N * GW,
                            (uint32_t)(N * GW * sizeof(double2)));
     }
   };
+  double Dreg[RSG ? RB : 1];
+  if constexpr (RSG) {
+    if (threadIdx.x == 0) {
+      mbar_init(&rbar, 1);
+    }
+    __syncthreads();
+    issue_r(0);
+  }
   stage(0);
   prefetch_r(0);
-  mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
+  if constexpr (RSG) {
+    // slots, and this thread's diagonal values D[blk*RB + e][s] from the plan's table
+    __shared__ int s_dc;
+    mid_slots<N, G, W>(cg0, pl, s_k1, s_k2, s_wgt, s_tw);
+    if (threadIdx.x == 0) s_dc = -1;
+    __syncthreads();
+    if (MODE != MID_APPLY && threadIdx.x < GW && s_k1[threadIdx.x] == 0 && s_k2[threadIdx.x] == 0)
+      s_dc = threadIdx.x;
+    __syncthreads();
+    const int s = threadIdx.x % GW, blk = threadIdx.x / GW;
+    const double* Dg = pl.D + (size_t)(cg0 / W) * N * GW + (blk * RB) * GW + s;
+#pragma unroll
+    for (int e = 0; e < RB; ++e) Dreg[e] = (blk * RB + e == 0 && s == s_dc) ? 0.0 : __ldg(Dg + e * GW);
+  } else {
+    mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
+  }
 
   const double scale = 2.0 / ((double)N * N * N);
   const int ntab = N;
@@ -1500,9 +1541,29 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
       const double wgt = s_wgt[s];
       const double al = s_alpha[c * P + pr];
       double2* Rt = ctl.Rh + ((size_t)(b0 + c * P + pr) * TILES + tile) * N * GW + (blk * RB) * GW + s;
+      if constexpr (RSG) {
+        if (MODE == MID_ITER) {
+          mbar_wait(&rbar, rphase & 1);
+          const double2* Rs = rstg + (blk * RB) * GW + s;
 #pragma unroll
-      for (int e = 0; e < RB; ++e)
-        v[e] = mid_point<MODE>(v[e], Dsm[(blk * RB + e) * GW + s], wgt, scale, al, Rt + e * GW, rr, rz);
+          for (int e = 0; e < RB; ++e) {  // mid_point<MID_ITER> with the residual from smem
+            const double2 Ro = Rs[e * GW];
+            const double2 R = make_double2(fma(-al, v[e].x, Ro.x), fma(-al, v[e].y, Ro.y));
+            Rt[e * GW] = R;
+            const double m2 = R.x * R.x + R.y * R.y;
+            rr = fma(wgt, m2, rr);
+            rz = fma(wgt * Dreg[e], m2, rz);
+            v[e] = cscale(R, Dreg[e] * scale);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < RB; ++e) v[e] = mid_point<MODE>(v[e], Dreg[e], wgt, scale, al, Rt + e * GW, rr, rz);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < RB; ++e)
+          v[e] = mid_point<MODE>(v[e], Dsm[(blk * RB + e) * GW + s], wgt, scale, al, Rt + e * GW, rr, rz);
+      }
 #pragma unroll
       for (int pr2 = 0; pr2 < P; ++pr2)
         if (pr2 == pr) {
@@ -1514,6 +1575,10 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
       for (int e = 0; e < RB; ++e) row[e * RS] = v[e];
     }
     __syncthreads();
+    if constexpr (RSG) {  // the residual buffer is free again: fetch the next realization's tile
+      if (MODE == MID_ITER && s_act[c]) ++rphase;
+      issue_r(c + 1);
+    }
     // ---- phase A inverse: smem -> registers -> global ----
     for (int item = threadIdx.x; item < P * ITEMS_A; item += blockDim.x) {
       const int pr = item / ITEMS_A, ia = item - pr * ITEMS_A;
