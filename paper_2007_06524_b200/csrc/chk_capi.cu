@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <string>
 #include <thread>
 #include <type_traits>
@@ -924,8 +925,17 @@ int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, c
   if (lanes == 1) {
     lane_fn(0);
   } else {
+    // lane 0 runs on the calling thread; no exception may cross the C ABI
     std::vector<std::thread> th;
-    for (int l = 0; l < lanes; ++l) th.emplace_back(lane_fn, l);
+    try {
+      for (int l = 1; l < lanes; ++l) th.emplace_back(lane_fn, l);
+    } catch (const std::exception& ex) {
+      for (int l = 1 + (int)th.size(); l < lanes; ++l) {
+        out[l].rc = CHK_ECUDA;
+        out[l].err = std::string("cannot start a pipeline lane: ") + ex.what();
+      }
+    }
+    lane_fn(0);
     for (auto& t : th) t.join();
   }
   cudaEventDestroy(start);
