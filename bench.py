@@ -216,6 +216,10 @@ def run_ours(args):
     lib.chk_profile_read(prof_ms.ctypes.data_as(ctypes.c_void_p), prof_n.ctypes.data_as(ctypes.c_void_p))
     lib.chk_profile_enable(0)
 
+    # --- the two operators stand-alone (north_star: >= 60 % of the HBM roofline
+    # for the matvec and the preconditioner apply at n >= 128), same batch ------
+    standalone = standalone_ops(lib, A, F, U, P, args.steps, torch)
+
     # --- e2e: reference-facing call with host buffers --------------------------
     # chk_pcg_solve_host: pinned numpy-side inputs/outputs, the batch streamed
     # through the GPU in 4 chunks with H2D / D2H overlapped with the solves
@@ -322,6 +326,7 @@ def run_ours(args):
             "e2e": {"value": e2e_dof_total / (e2e_max / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
                     "ms_per_step": e2e_max},
+            "standalone": standalone,
             "gpu_launches": int(launches_total),
             "clocks": clk,
             "cpu_baseline": cpu,
@@ -329,6 +334,48 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def standalone_ops(lib, A, F, Y, P, reps, torch):
+    """Event-timed chk_stencil_apply (y = A x with <x, y>; reads x, writes y, plus
+    the L^3 cells: 16 + 8 L^3/n^3 B/DOF) and chk_precond_apply (z = P r through
+    the forward plane, middle and inverse passes: 8 + 4 x 8.1 + 8 = 48.5 B/DOF)
+    over the whole batch, on the current stream, after one warm-up launch."""
+    B, nb = F.shape
+    n = round(nb ** (1.0 / 3.0))
+    peak, _ = measured_peaks()
+    stream = torch.cuda.current_stream()
+    vp = ctypes.c_void_p
+    xy = torch.empty(B, dtype=torch.float64, device=F.device)
+    wsb = int(lib.chk_precond_workspace_bytes(P.plan.handle, B))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=F.device)
+    spec = 8.0 * (n // 2 + 1) / (n // 2)
+    cells = 8.0 * A.beta.shape[1] / nb
+    ops = {
+        "stencil_apply": (16.0 + cells, lambda: lib.chk_stencil_apply(
+            ctypes.byref(A.grid), vp(A.beta.data_ptr()), vp(F.data_ptr()), vp(Y.data_ptr()),
+            vp(xy.data_ptr()), B, vp(stream.cuda_stream))),
+        "precond_apply": (16.0 + 4.0 * spec, lambda: lib.chk_precond_apply(
+            P.plan.handle, vp(F.data_ptr()), vp(Y.data_ptr()), B, vp(ws.data_ptr()), wsb,
+            vp(stream.cuda_stream))),
+    }
+    out = {}
+    for name, (bpd, call) in ops.items():
+        assert call() == 0, name
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            assert call() == 0, name
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = bpd * B * nb / (ms / 1e3) / 1e9
+        out[name] = {"ms_per_launch": round(ms, 3), "alg_bytes_per_dof": round(bpd, 3),
+                     "achieved_gbs": round(gbs, 1), "peak_gbs": peak, "frac": round(gbs / peak, 3),
+                     "dof_per_launch": int(B * nb)}
+    del ws
+    return out
 
 
 # ---------------------------------------------------------------------------

@@ -636,13 +636,37 @@ int32_t chk_stencil_apply(const chk_grid* grid, const double* beta, const double
   double* part = nullptr;
   unsigned* cnt = nullptr;
   if (xy) {
+    // per-CTA partials + tickets of <x, y>: a per-thread scratch buffer kept across
+    // calls (grown on demand; the tickets are zeroed in stream order every call)
+    struct Scratch {
+      int dev = -1;
+      void* p = nullptr;
+      size_t cap = 0;
+      ~Scratch() {
+        if (p) cudaFree(p);
+      }
+    };
+    static thread_local Scratch sc;
+    int dev = 0;
+    CHK_CUDA(cudaGetDevice(&dev));
     const size_t pb = sizeof(double) * 2 * (size_t)grid->n * 16 * B;  // N*G <= 16 n
-    CHK_CUDA(cudaMallocAsync(&part, pb + sizeof(unsigned) * B, s));
-    cnt = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(part) + pb);
+    const size_t need = pb + sizeof(unsigned) * B;
+    if (sc.cap < need || sc.dev != dev) {
+      if (sc.p) {
+        CHK_CUDA(cudaStreamSynchronize(s));  // earlier calls on this thread may still use it
+        cudaFree(sc.p);
+        sc.p = nullptr;
+        sc.cap = 0;
+      }
+      CHK_CUDA(cudaMalloc(&sc.p, need));
+      sc.cap = need;
+      sc.dev = dev;
+    }
+    part = static_cast<double*>(sc.p);
+    cnt = reinterpret_cast<unsigned*>(static_cast<char*>(sc.p) + pb);
     CHK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * B, s));
   }
   CHK_DISPATCH(grid->n, { rc = O::stencil(s, B, g, beta, x, y, xy, part, cnt); });
-  if (part) CHK_CUDA(cudaFreeAsync(part, s));
   return rc;
 }
 

@@ -519,6 +519,17 @@ __device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
   stencil4_allin_q(g.lam, pc, xm, xp, ym, yp, pl, prr, m00, m01, m10, m11, z00, z01, z10, z11, q);
 }
 
+__device__ __forceinline__ void ldv4(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p)
+               : "memory");
+}
+__device__ __forceinline__ void stv4(double* p, const double (&v)[4]) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+
 // Quad (4 consecutive doubles of a smem row, x2s % 4 == 0) as two 16-byte
 // accesses in a swizzled order: quads 4i..4i+3 start with their low half, quads
 // 4i+4..4i+7 with their high half, so a warp's 32 consecutive quads (32-byte
@@ -547,7 +558,9 @@ __device__ __forceinline__ void ld_quad_smem(const double* rowp, int x2s, double
 // 4 (3) row loads per step instead of 5.  The cell values of x2s - 1 come from
 // lane - 1 by shuffle (the quad is one aligned 4-node run inside a cell, n0 >= 4).
 // Same formulas as stencil4_allin; q goes to the smem row of t, <p, q> into acc.
-template <int N, int G, int NR>
+// out: shared rows (pitch rowpitch, row index t) or, with OUTG, the global plane
+// x0 of the result (row x1, 32-byte stores).
+template <int N, int G, int NR, bool OUTG = false>
 __device__ __forceinline__ void stencil_march(const Geo& g, const Planes& P3, const double* __restrict__ beta,
                                               int x0, int gg, double* sm, int rowpitch, double& acc) {
   constexpr int nm = N - 1;
@@ -590,7 +603,11 @@ __device__ __forceinline__ void stencil_march(const Geo& g, const Planes& P3, co
     const double prr = __shfl_sync(0xffffffffu, pc[0], (lane + 1) & (Q4 - 1), Q4);
     double q[4];
     stencil4_allin_q(g.lam, pc, xm, xp, ym, yp, pl, prr, m00, m01, m10, m11, z00, z01, z10, z11, q);
-    st_quad_smem(sm + t * rowpitch, x2s, q);
+    if constexpr (OUTG) {
+      stv4(sm + (size_t)x1 * N + x2s, q);
+    } else {
+      st_quad_smem(sm + t * rowpitch, x2s, q);
+    }
     acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -633,15 +650,19 @@ __global__ void __launch_bounds__(256) stencil_apply_kernel(Geo g, const double*
   const Planes P3 = periodic_planes(xb, x0, N);
   double acc = 0.0;
   constexpr int Q4 = N / 4;
-  for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
-    const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
-    const int x1 = gg + G * t;
-    double pc[4], q[4];
-    stencil_quad<N, ALLIN>(g, P3, bb, x0, x1, x2, pc, q);
-    double2* yo = reinterpret_cast<double2*>(y + b * nb + ((size_t)x0 * N + x1) * N + x2);
-    yo[0] = make_double2(q[0], q[1]);
-    yo[1] = make_double2(q[2], q[3]);
-    acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
+  if (CHK_FWD_PF && threadIdx.x < NR)  // this CTA's rows of x: start the DRAM reads now
+    bulk_prefetch_l2(P3.c + (size_t)(gg + G * threadIdx.x) * N, N * sizeof(double));
+  if constexpr (ALLIN && CHK_MARCH && (Q4 == 16 || Q4 == 32) && G <= 2) {
+    stencil_march<N, G, NR, true>(g, P3, bb, x0, gg, y + b * nb + (size_t)x0 * N * N, 0, acc);
+  } else {
+    for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
+      const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
+      const int x1 = gg + G * t;
+      double pc[4], q[4];
+      stencil_quad<N, ALLIN>(g, P3, bb, x0, x1, x2, pc, q);
+      stv4(y + b * nb + ((size_t)x0 * N + x1) * N + x2, q);
+      acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
+    }
   }
   if (xy != nullptr) {
     double t0, t1;
@@ -779,17 +800,6 @@ __device__ __forceinline__ void ld4v(const double* p, double (&v)[4]) {
                : "l"(p));
 }
 
-__device__ __forceinline__ void ldv4(const double* p, double (&v)[4]) {
-  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
-               : "l"(p)
-               : "memory");
-}
-__device__ __forceinline__ void stv4(double* p, const double (&v)[4]) {
-  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
-               : "memory");
-}
-
 // CTA body, `bid` = plane block index (blockIdx.x of the stand-alone kernel)
 template <int N, int G, int MODE, bool ALLIN>
 __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __restrict__ beta,
@@ -815,18 +825,26 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   constexpr int Q4 = N / 4;
 
   if (MODE == FWD_APPLY) {
-    for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
-      const int t = i / N, x2 = i - (i / N) * N;
-      sm[t * 2 * HP + x2] = __ldg(src + b * nb + ((size_t)x0l * N + gg + G * t) * N + x2);
+    // rows of x -> smem rows, 32 bytes per thread
+    for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
+      const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
+      double v[4];
+      ldg4v(src + b * nb + ((size_t)x0l * N + gg + G * t) * N + x2, v);
+      st_quad_smem(sm + t * 2 * HP, x2, v);
     }
   } else if (MODE == FWD_INIT) {
     const int status = st->status;
     const double shift = st->rhs_projected ? st->mean_f : 0.0;  // solver.py:139-143
-    for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
-      const int t = i / N, x2 = i - (i / N) * N;
+    for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
+      const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
       const size_t idx = b * nb + ((size_t)x0l * N + gg + G * t) * N + x2;
-      u[idx] = 0.0;
-      sm[t * 2 * HP + x2] = __ldg(src + idx) - shift;
+      double v[4];
+      ldg4v(src + idx, v);
+      const double zero[4] = {0.0, 0.0, 0.0, 0.0};
+      stv4(u + idx, zero);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] -= shift;
+      st_quad_smem(sm + t * 2 * HP, x2, v);
     }
     if (status != ST_ACTIVE) return;
   } else {  // FWD_Q
