@@ -694,13 +694,6 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
                               int32_t* status, int32_t* rhs_projected, double* history,
                               void* workspace, size_t workspace_bytes, void* stream) {
   g_launches = 0;
-  if (const char* e = getenv("CHK_L2FETCH")) {  // experiment: L2 fetch granularity (bytes)
-    static bool done = false;
-    if (!done) {
-      cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
-      done = true;
-    }
-  }
   Geo g;
   int rc = check_grid(grid, &g);
   if (rc) return rc;
