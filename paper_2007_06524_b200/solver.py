@@ -215,7 +215,9 @@ def pcg_solve_host(config, beta_host, F_host, opts: SolveOptions | None = None,
     Fh = Fh.reshape(B, -1).contiguous()
     U = out if out is not None else torch.empty_like(Fh)
     if chunk is None:
-        chunk = max(1, (B + 7) // 8)  # 3 lanes x chunks of B/8 (measured best for config 3)
+        # 3 lanes x chunks of B/8, but at least ~4M DOF per chunk (per-solve overheads):
+        # measured best for configs 2, 3, 4 (16, 32, 2 realizations)
+        chunk = max(1, (B + 7) // 8, -(-(4 << 20) // n ** 3))
     grid = _lib.grid_struct(3, n, config.L, config.n0, config.k, config.offset, config.lam)
     lib = _lib.load()
     wb = int(lib.chk_pcg_host_workspace_bytes(ctypes.byref(grid), plan.handle, min(chunk, B), opts.max_iter))
