@@ -243,6 +243,12 @@ struct Ops {
       if (SX) sm += (size_t)G * RA * NT * sizeof(double2);
       CHK_CUDA(allow_smem(mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT, SX>, sm));
       mid_column_reg_kernel<N, G, W, RA, NBX, PX, MODE, NT, SX><<<grid, NT, sm, s>>>(S, pl, ctl, sg, it, B);
+    } else if (N == 256 && CHK_R256) {
+      // register-phase kernel (x0 radix order 2, 8, 8, 2; diagonal from the plan table)
+      if (!pl.D) return fail(CHK_EINVAL, "n = 256 middle pass needs the plan's diagonal table");
+      const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
+      CHK_CUDA(allow_smem(mid_column_r256_kernel<NBX, MODE>, sm));
+      mid_column_r256_kernel<NBX, MODE><<<grid, 256, sm, s>>>(S, pl, ctl, sg, it, B);
     } else if (pl.D && mid_dg()) {
       const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
       CHK_CUDA(allow_smem(mid_column_fused_kernel<N, G, W, NBX, MODE, true>, sm));
@@ -467,11 +473,11 @@ static PlanDev plan_dev(const chk_precond_plan* p) {
   return PlanDev{p->d_tw, p->d_U, p->d_Up, p->d_lam, p->r1, p->kind, p->delta, p->d_D};
 }
 
-// host copy of dig_freq (chk_kernels.cuh): frequency stored at digit-reversed position p
+// host copy of dig_freq0 (chk_kernels.cuh): frequency stored at x0 position p
 static int host_dig_freq(int N, int p) {
   int k = 0, mul = 1, M = N;
   while (M > 1) {
-    const int R = (M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2);
+    const int R = x0_radix(N, M);
     const int Mn = M / R;
     const int m = p / Mn;
     p -= m * Mn;
@@ -572,7 +578,8 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
   }
   // diagonal tiles of every middle-pass tile (n^2 (n/2+1) doubles: 8.5 MB at
   // n = 128, 539 MB at n = 512); CHK_NO_DTILE=1 evaluates them per CTA instead
-  if (!(getenv("CHK_NO_DTILE") && atoi(getenv("CHK_NO_DTILE")))) {
+  // (n = 256 always has the table: its middle pass reads it)
+  if (!(getenv("CHK_NO_DTILE") && atoi(getenv("CHK_NO_DTILE"))) || (n == 256 && CHK_R256)) {
     const int rc2 = plan_dtiles(p);
     if (rc2) {
       chk_precond_plan_destroy(p);

@@ -209,6 +209,35 @@ __device__ __forceinline__ int dig_freq(int p) {
   return k;
 }
 
+// x0-axis radix policy of the middle pass.  n = 256 (CHK_R256): 2, 8, 8, 2 -- a
+// radix-2 first stage lets the group combine and that stage share registers
+// (mid_column_r256_kernel); every other length uses the generic 8, 4, 2 rule.
+#ifndef CHK_R256
+#define CHK_R256 1
+#endif
+__host__ __device__ constexpr int x0_radix(int N, int M) {
+  return (N == 256 && CHK_R256) ? ((M == 256 || M == 2) ? 2 : 8)
+                                : ((M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2));
+}
+// frequency held at position p after the forward x0 transform (x0_radix order)
+template <int N>
+__device__ __forceinline__ int dig_freq0(int p) {
+  int k = 0, mul = 1;
+  int M = N;
+#pragma unroll
+  for (int s = 0; s < 12; ++s) {
+    if (M <= 1) break;
+    const int R = x0_radix(N, M);
+    const int Mn = M / R;
+    const int m = p / Mn;
+    p -= m * Mn;
+    k += m * mul;
+    mul *= R;
+    M = Mn;
+  }
+  return k;
+}
+
 // ----------------------------------------------------------------------------
 // last-block reduction of two scalars per realization
 // ----------------------------------------------------------------------------
@@ -1078,7 +1107,7 @@ __device__ __forceinline__ void mid_dtile(double* coef, double* Dsm, const PlanD
   } else {
     for (int i = threadIdx.x; i < N * GW; i += blockDim.x) {
       const int s = i % GW, pos0 = i / GW;
-      const int k0 = dig_freq<N>(pos0);
+      const int k0 = dig_freq0<N>(pos0);
       // eigensum order of spectral.py:47-52: (lam_i + lam_j) + lam_k
       const double gsum = (__ldg(pl.lam + k0) + __ldg(pl.lam + s_k1[s])) + __ldg(pl.lam + s_k2[s]);
       double D;
@@ -1316,6 +1345,185 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
       for (int g = 1; g < G; ++g) v[g] = cmulc(v[g], s_tw[g * W + w]);
 #pragma unroll
       for (int g = 0; g < G; ++g) S[rbase + (size_t)g * GSTR] = v[g];
+    }
+    if (MODE != MID_APPLY) warp_partials(rr, rz, s_wsum, j);
+    __syncthreads();
+  }
+  if (MODE != MID_APPLY) {
+    const double inv = 1.0 / ((double)N * N * N);  // Parseval: (1/N^3) sum conj(X) Y
+    mid_tickets<NB>(s_wsum, s_act, b0, tile, TILES, ctl, scratch, [&](int b, double t0, double t1) {
+      mid_decide(ctl.st + b, ctl, b, it, t0 * inv, t1 * inv);
+    });
+  }
+}
+
+// ----------------------------------------------------------------------------
+// kernel 2c: register-phase spectral column pass for n = 256 (x0 radix 2, 8, 8, 2)
+// ----------------------------------------------------------------------------
+// CTA = NB realizations x one tile (W = 2 columns x G = 8 groups = 16 slots, 256
+// x0 positions; interleaved spectrum layout).  Per realization:
+//   A  (thread = column w, x0 pair j, j + 128): group combine of both x0 rows in
+//      registers + the radix-2 x0 stage (M = 256)                     -> smem
+//   B1 (thread = slot, block, offset): radix-8 stage M = 128            smem -> smem
+//   B2 (thread = slot, 16-block): radix-8 (M = 16) + radix-2 (M = 2), residual
+//      update / diagonal (read from the plan's table) / Parseval, inverse   smem -> smem
+//   B1' inverse M = 128 stage;  A' inverse radix-2 + group combine      -> HBM
+// 8 shared-memory passes per element (the stage kernel mid_column_fused: 12).
+template <int NB, int MODE>
+#ifndef CHK_R256_MINB
+#define CHK_R256_MINB 2
+#endif
+__global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(double2* __restrict__ S, PlanDev pl, SolveCtl ctl,
+                                                                 SlabGeo sg, int it, int B) {
+  constexpr int N = 256, G = 8, W = 2, GW = G * W, RS = GW + 1;
+  static_assert(IlW<N>::value == W, "interleaved spectrum layout expected at n = 256");
+  static_assert(x0_radix(N, 256) == 2 && x0_radix(N, 128) == 8 && x0_radix(N, 16) == 8 && x0_radix(N, 2) == 2,
+                "x0 radix order 2, 8, 8, 2");
+  const int TILES = sg.tiles;
+  const int nsh = __ffs(sg.nloc) - 1;
+  extern __shared__ double2 buf[];  // [N][RS]
+  __shared__ double scratch[64];
+  __shared__ int s_k1[GW], s_k2[GW];
+  __shared__ double s_wgt[GW];
+  __shared__ double2 s_tw[GW];
+  __shared__ int s_act[NB];
+  __shared__ double s_alpha[NB];
+  __shared__ double s_wsum[NB * 8 * 2];
+  __shared__ int s_dc;
+  const int bg = blockIdx.x / TILES;
+  const int tile = blockIdx.x - bg * TILES;
+  const int c0 = tile * W;
+  const int cg0 = (sg.tile_off + tile) * W;
+  const int b0 = bg * NB;
+  if (threadIdx.x == 0) {
+    int any = 0;
+    for (int j = 0; j < NB; ++j) {
+      const int b = b0 + j;
+      int a = (b < B);
+      if (a && MODE != MID_APPLY) a = (ctl.st[b].status == ST_ACTIVE);
+      s_act[j] = a;
+      s_alpha[j] = (a && MODE == MID_ITER) ? ctl.st[b].alpha : 0.0;
+      any |= a;
+    }
+    scratch[0] = any;
+    s_dc = -1;
+  }
+  __syncthreads();
+  if (scratch[0] == 0.0) return;
+  mid_slots<N, G, W>(cg0, pl, s_k1, s_k2, s_wgt, s_tw);
+  __syncthreads();
+  if (MODE != MID_APPLY && threadIdx.x < GW && s_k1[threadIdx.x] == 0 && s_k2[threadIdx.x] == 0)
+    s_dc = threadIdx.x;
+  __syncthreads();
+  const double* Dg = pl.D + (size_t)(cg0 / W) * N * GW;
+  const double scale = 2.0 / ((double)N * N * N);
+  const int wA = threadIdx.x & 1, jA = threadIdx.x >> 1;  // phase A item (column, x0 pair)
+  for (int j = 0; j < NB; ++j) {
+    if (!s_act[j]) continue;
+    const int b = b0 + j;
+    // ---- A: loads, group combine, radix-2 stage (M = 256) ----
+    {
+      double2 v[2][G];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int x0 = jA + 128 * h;
+        const size_t rbase = slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), 0) + c0 * G + wA;
+#pragma unroll
+        for (int g = 0; g < G; ++g) v[h][g] = S[rbase + (size_t)g * W];
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int g = 1; g < G; ++g) v[h][g] = cmul(v[h][g], s_tw[g * W + wA]);
+        reg_fft<G, false>(v[h], pl.tw, N);
+      }
+      const double2 t1 = __ldg(pl.tw + jA);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double2 a = cadd(v[0][g], v[1][g]);
+        const double2 d = cmul(csub(v[0][g], v[1][g]), t1);
+        buf[jA * RS + g * W + wA] = a;
+        buf[(jA + 128) * RS + g * W + wA] = d;
+      }
+    }
+    __syncthreads();
+    // ---- B1: radix-8 stage M = 128 (stride 16) ----
+    for (int item = threadIdx.x; item < 2 * 16 * GW; item += blockDim.x) {
+      const int s = item % GW, jj = (item / GW) % 16, blk = item / (16 * GW);
+      double2* base = buf + (blk * 128 + jj) * RS + s;
+      double2 v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = base[16 * t * RS];
+      dftR<8, false>(v);
+      if (jj > 0) {
+#pragma unroll
+        for (int m = 1; m < 8; ++m) v[m] = cmul(v[m], __ldg(pl.tw + jj * m * 2));
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) base[16 * t * RS] = v[t];
+    }
+    __syncthreads();
+    // ---- B2: last two stages, residual / diagonal / Parseval, first two inverse stages ----
+    double rr = 0.0, rz = 0.0;
+    {
+      const int s = threadIdx.x % GW, blk = threadIdx.x / GW;  // 16 blocks of 16 positions
+      double2* row = buf + (blk * 16) * RS + s;
+      double2 v[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = row[e * RS];
+      reg_fft<16, false>(v, pl.tw, N);
+      double2* Rt = ctl.Rh + ((size_t)b * TILES + tile) * N * GW + (blk * 16) * GW + s;
+      const double wgt = s_wgt[s];
+      const double al = s_alpha[j];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int pos0 = blk * 16 + e;
+        // mean projection of z (solver.py:153,179): the zero-frequency coefficient is 0
+        const double D = (pos0 == 0 && s == s_dc) ? 0.0 : __ldg(Dg + pos0 * GW + s);
+        v[e] = mid_point<MODE>(v[e], D, wgt, scale, al, Rt + e * GW, rr, rz);
+      }
+      reg_fft<16, true>(v, pl.tw, N);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) row[e * RS] = v[e];
+    }
+    __syncthreads();
+    // ---- B1': inverse M = 128 stage ----
+    for (int item = threadIdx.x; item < 2 * 16 * GW; item += blockDim.x) {
+      const int s = item % GW, jj = (item / GW) % 16, blk = item / (16 * GW);
+      double2* base = buf + (blk * 128 + jj) * RS + s;
+      double2 v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = base[16 * t * RS];
+      if (jj > 0) {
+#pragma unroll
+        for (int m = 1; m < 8; ++m) v[m] = cmulc(v[m], __ldg(pl.tw + jj * m * 2));
+      }
+      dftR<8, true>(v);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) base[16 * t * RS] = v[t];
+    }
+    __syncthreads();
+    // ---- A': inverse radix-2 stage, inverse group combine, store ----
+    {
+      double2 v[2][G];
+      const double2 t1 = __ldg(pl.tw + jA);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double2 a = buf[jA * RS + g * W + wA];
+        const double2 d = cmulc(buf[(jA + 128) * RS + g * W + wA], t1);
+        v[0][g] = cadd(a, d);
+        v[1][g] = csub(a, d);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        reg_fft<G, true>(v[h], pl.tw, N);
+#pragma unroll
+        for (int g = 1; g < G; ++g) v[h][g] = cmulc(v[h][g], s_tw[g * W + wA]);
+        const int x0 = jA + 128 * h;
+        const size_t rbase = slab_row(sg, B, G, x0 >> nsh, b, x0 & (sg.nloc - 1), 0) + c0 * G + wA;
+#pragma unroll
+        for (int g = 0; g < G; ++g) S[rbase + (size_t)g * W] = v[h][g];
+      }
     }
     if (MODE != MID_APPLY) warp_partials(rr, rz, s_wsum, j);
     __syncthreads();
