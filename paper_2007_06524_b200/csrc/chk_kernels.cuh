@@ -1370,6 +1370,9 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
 //   B1' inverse M = 128 stage;  A' inverse radix-2 + group combine      -> HBM
 // 8 shared-memory passes per element (the stage kernel mid_column_fused: 12).
 template <int NB, int MODE>
+#ifndef CHK_R256_RPF
+#define CHK_R256_RPF 1
+#endif
 #ifndef CHK_R256_MINB
 #define CHK_R256_MINB 2
 #endif
@@ -1421,6 +1424,8 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
   for (int j = 0; j < NB; ++j) {
     if (!s_act[j]) continue;
     const int b = b0 + j;
+    if (CHK_R256_RPF && MODE == MID_ITER && threadIdx.x == 0)  // residual tile -> L2 before B2 reads it
+      bulk_prefetch_l2(ctl.Rh + ((size_t)b * TILES + tile) * N * GW, (uint32_t)(N * GW * sizeof(double2)));
     // ---- A: loads, group combine, radix-2 stage (M = 256) ----
     {
       double2 v[2][G];
