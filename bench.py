@@ -294,7 +294,8 @@ def run_ours(args):
             # ncu --set full dram__bytes_read+write of the same kernel (profiles/), per DOF,
             # scaled to the DOF one launch processes on average in this run
             ncu_name = {"fwd_plane": "fwd_plane_kernel",
-                        "mid_column": "mid_column_reg_kernel" if n <= 128 else "mid_column_fused_kernel",
+                        "mid_column": ("mid_column_reg_kernel" if n <= 128 else
+                                       "mid_column_r256_kernel" if n == 256 else "mid_column_fused_kernel"),
                         "inv_plane": "inv_plane_kernel", "plane_pair": "pair_plane_kernel"}.get(dom)
             tj = json.load(open(prof_json)).get(f"config{cfg_id}", {}).get(ncu_name)
             if tj:
