@@ -509,7 +509,19 @@ __device__ __forceinline__ void stencil4_allin_q(double lam, const double (&pc)[
   }
 }
 
-template <int N>
+// Cell values of the four cell rows (c0m|c00) x (c1m|c10) at cell column c: rows
+// coincide when x0 - 1 (x1 - 1) lies in the same cell as x0 (x1) -- 3 of 4 node
+// planes / rows at n0 = 4 -- and are then loaded once (same values, same bits).
+__device__ __forceinline__ void cell4(const double* b00, const double* b01, const double* b10, const double* b11,
+                                      bool s0, bool s1, int c, double& v00, double& v01, double& v10,
+                                      double& v11) {
+  v11 = __ldg(b11 + c);
+  v10 = s1 ? v11 : __ldg(b10 + c);
+  v01 = s0 ? v11 : __ldg(b01 + c);
+  v00 = s0 ? v10 : (s1 ? v01 : __ldg(b00 + c));
+}
+
+template <int N, bool DEDUP = false>
 __device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
                                                const double* __restrict__ beta, int x0, int x1,
                                                int x2s, double (&pc)[4], double (&q)[4]) {
@@ -543,8 +555,12 @@ __device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
   const double* b01 = beta + ((size_t)c0m * L + c10) * L;  // (x0-1, x1)
   const double* b10 = beta + ((size_t)c00 * L + c1m) * L;  // (x0,   x1-1)
   const double* b11 = beta + ((size_t)c00 * L + c10) * L;  // (x0,   x1)
-  const double m00 = __ldg(b00 + cm), m01 = __ldg(b01 + cm), m10 = __ldg(b10 + cm), m11 = __ldg(b11 + cm);
-  const double z00 = __ldg(b00 + cc), z01 = __ldg(b01 + cc), z10 = __ldg(b10 + cc), z11 = __ldg(b11 + cc);
+  // DEDUP: coinciding cell rows loaded once (fewer loads, more live registers:
+  // pays in the stand-alone stencil, not inside the register-bound plane passes)
+  const bool s0 = DEDUP && (c0m == c00), s1 = DEDUP && (c1m == c10);
+  double m00, m01, m10, m11, z00, z01, z10, z11;
+  cell4(b00, b01, b10, b11, s0, s1, cm, m00, m01, m10, m11);
+  cell4(b00, b01, b10, b11, s0, s1, cc, z00, z01, z10, z11);
   stencil4_allin_q(g.lam, pc, xm, xp, ym, yp, pl, prr, m00, m01, m10, m11, z00, z01, z10, z11, q);
 }
 
@@ -589,7 +605,7 @@ __device__ __forceinline__ void ld_quad_smem(const double* rowp, int x2s, double
 // Same formulas as stencil4_allin; q goes to the smem row of t, <p, q> into acc.
 // out: shared rows (pitch rowpitch, row index t) or, with OUTG, the global plane
 // x0 of the result (row x1, 32-byte stores).
-template <int N, int G, int NR, bool OUTG = false>
+template <int N, int G, int NR, bool OUTG = false, bool DEDUP = false>
 __device__ __forceinline__ void stencil_march(const Geo& g, const Planes& P3, const double* __restrict__ beta,
                                               int x0, int gg, double* sm, int rowpitch, double& acc) {
   constexpr int nm = N - 1;
@@ -624,7 +640,8 @@ __device__ __forceinline__ void stencil_march(const Geo& g, const Planes& P3, co
     const double* b01 = beta + ((size_t)c0m * L + c10) * L;
     const double* b10 = beta + ((size_t)c00 * L + c1m) * L;
     const double* b11 = beta + ((size_t)c00 * L + c10) * L;
-    const double z00 = __ldg(b00 + cc), z01 = __ldg(b01 + cc), z10 = __ldg(b10 + cc), z11 = __ldg(b11 + cc);
+    double z00, z01, z10, z11;
+    cell4(b00, b01, b10, b11, DEDUP && c0m == c00, DEDUP && c1m == c10, cc, z00, z01, z10, z11);
     const int src = (lane - 1) & (Q4 - 1);
     const double m00 = __shfl_sync(0xffffffffu, z00, src, Q4), m01 = __shfl_sync(0xffffffffu, z01, src, Q4);
     const double m10 = __shfl_sync(0xffffffffu, z10, src, Q4), m11 = __shfl_sync(0xffffffffu, z11, src, Q4);
@@ -650,12 +667,12 @@ __device__ __forceinline__ void stencil_march(const Geo& g, const Planes& P3, co
   }
 }
 
-template <int N, bool ALLIN>
+template <int N, bool ALLIN, bool DEDUP = false>
 __device__ __forceinline__ void stencil_quad(const Geo& g, const Planes& P3,
                                              const double* __restrict__ beta, int x0, int x1,
                                              int x2s, double (&pc)[4], double (&q)[4]) {
   if constexpr (ALLIN) {
-    stencil4_allin<N>(g, P3, beta, x0, x1, x2s, pc, q);
+    stencil4_allin<N, DEDUP>(g, P3, beta, x0, x1, x2s, pc, q);
   } else {
     const RowCtx rc = make_row(P3, beta, g, x0, x1);
     stencil4(g, rc, x2s, pc, q);
@@ -682,13 +699,13 @@ __global__ void __launch_bounds__(256) stencil_apply_kernel(Geo g, const double*
   if (CHK_FWD_PF && threadIdx.x < NR)  // this CTA's rows of x: start the DRAM reads now
     bulk_prefetch_l2(P3.c + (size_t)(gg + G * threadIdx.x) * N, N * sizeof(double));
   if constexpr (ALLIN && CHK_MARCH && (Q4 == 16 || Q4 == 32) && G <= 2) {
-    stencil_march<N, G, NR, true>(g, P3, bb, x0, gg, y + b * nb + (size_t)x0 * N * N, 0, acc);
+    stencil_march<N, G, NR, true, true>(g, P3, bb, x0, gg, y + b * nb + (size_t)x0 * N * N, 0, acc);
   } else {
     for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
       const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
       const int x1 = gg + G * t;
       double pc[4], q[4];
-      stencil_quad<N, ALLIN>(g, P3, bb, x0, x1, x2, pc, q);
+      stencil_quad<N, ALLIN, (N == 512)>(g, P3, bb, x0, x1, x2, pc, q);  // (n = 256: -8 % with dedup)
       stv4(y + b * nb + ((size_t)x0 * N + x1) * N + x2, q);
       acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
     }
@@ -893,7 +910,7 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
       for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
         const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
         double pc[4], q[4];
-        stencil_quad<N, ALLIN>(g, P3, bb, x0, gg + G * t, x2, pc, q);
+        stencil_quad<N, ALLIN, (N == 512)>(g, P3, bb, x0, gg + G * t, x2, pc, q);
         st_quad_smem(sm + t * 2 * HP, x2, q);
         acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
       }
