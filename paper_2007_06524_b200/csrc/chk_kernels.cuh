@@ -32,6 +32,9 @@
 #ifndef CHK_INV_PF  // L2 prefetch of the p / u rows at the start of the inverse pass (n <= 128;
 #define CHK_INV_PF 1    // at n >= 256 the prefetched rows are evicted before use: +38 % DRAM reads)
 #endif
+#ifndef CHK_MARCH_DEDUP  // cell-row de-duplication inside the plane passes' marching stencil
+#define CHK_MARCH_DEDUP 0
+#endif
 #ifndef CHK_MID_RPF
 #define CHK_MID_RPF 1
 #endif
@@ -905,7 +908,7 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
       bulk_prefetch_l2(P3.c + (size_t)(gg + G * threadIdx.x) * N, N * sizeof(double));
     double acc = 0.0;
     if constexpr (ALLIN && CHK_MARCH && (Q4 == 16 || Q4 == 32) && G <= 2) {
-      stencil_march<N, G, NR>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
+      stencil_march<N, G, NR, false, CHK_MARCH_DEDUP>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
     } else {
       for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
         const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
