@@ -32,6 +32,9 @@
 #ifndef CHK_INV_PF  // L2 prefetch of the p / u rows at the start of the inverse pass (n <= 128;
 #define CHK_INV_PF 1    // at n >= 256 the prefetched rows are evicted before use: +38 % DRAM reads)
 #endif
+#ifndef CHK_MARCH_S0  // marching stencil: specialised body for planes whose x0 - 1 is in the same cell
+#define CHK_MARCH_S0 1
+#endif
 #ifndef CHK_MARCH_DEDUP  // cell-row de-duplication inside the plane passes' marching stencil
 #define CHK_MARCH_DEDUP 0
 #endif
@@ -608,7 +611,10 @@ __device__ __forceinline__ void ld_quad_smem(const double* rowp, int x2s, double
 // Same formulas as stencil4_allin; q goes to the smem row of t, <p, q> into acc.
 // out: shared rows (pitch rowpitch, row index t) or, with OUTG, the global plane
 // x0 of the result (row x1, 32-byte stores).
-template <int N, int G, int NR, bool OUTG = false, bool DEDUP = false>
+// S0 / S1 (compile-time): the x0 - 1 and x0 cell planes coincide / the x1 - 1 and x1
+// cell rows coincide on every row of this CTA (caller checked), so those cell rows are
+// loaded once.
+template <int N, int G, int NR, bool OUTG = false, bool DEDUP = false, bool S0 = false, bool S1 = false>
 __device__ __forceinline__ void stencil_march(const Geo& g, const Planes& P3, const double* __restrict__ beta,
                                               int x0, int gg, double* sm, int rowpitch, double& acc) {
   constexpr int nm = N - 1;
@@ -644,7 +650,24 @@ __device__ __forceinline__ void stencil_march(const Geo& g, const Planes& P3, co
     const double* b10 = beta + ((size_t)c00 * L + c1m) * L;
     const double* b11 = beta + ((size_t)c00 * L + c10) * L;
     double z00, z01, z10, z11;
-    cell4(b00, b01, b10, b11, DEDUP && c0m == c00, DEDUP && c1m == c10, cc, z00, z01, z10, z11);
+    if constexpr (S0 && S1) {
+      z11 = __ldg(b11 + cc);
+      z10 = z11;
+      z01 = z11;
+      z00 = z11;
+    } else if constexpr (S0) {
+      z11 = __ldg(b11 + cc);
+      z10 = __ldg(b10 + cc);
+      z01 = z11;
+      z00 = z10;
+    } else if constexpr (S1) {
+      z11 = __ldg(b11 + cc);
+      z01 = __ldg(b01 + cc);
+      z10 = z11;
+      z00 = z01;
+    } else {
+      cell4(b00, b01, b10, b11, DEDUP && c0m == c00, DEDUP && c1m == c10, cc, z00, z01, z10, z11);
+    }
     const int src = (lane - 1) & (Q4 - 1);
     const double m00 = __shfl_sync(0xffffffffu, z00, src, Q4), m01 = __shfl_sync(0xffffffffu, z01, src, Q4);
     const double m10 = __shfl_sync(0xffffffffu, z10, src, Q4), m11 = __shfl_sync(0xffffffffu, z11, src, Q4);
@@ -908,7 +931,18 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
       bulk_prefetch_l2(P3.c + (size_t)(gg + G * threadIdx.x) * N, N * sizeof(double));
     double acc = 0.0;
     if constexpr (ALLIN && CHK_MARCH && (Q4 == 16 || Q4 == 32) && G <= 2) {
-      stencil_march<N, G, NR, false, CHK_MARCH_DEDUP>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
+      // s0: cell planes of x0 - 1 and x0 coincide; s1: every row x1 = gg + G t of this CTA
+      // shares its cell row with x1 - 1 (G = 2, odd gg, n0 >= 2)
+      const bool s0 = CHK_MARCH_S0 && ((((x0 - 1) & (N - 1)) >> g.sh) == (x0 >> g.sh));
+      const bool s1 = CHK_MARCH_S0 && G == 2 && (gg & 1) && g.sh >= 1;
+      if (s0 && s1)
+        stencil_march<N, G, NR, false, false, true, true>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
+      else if (s0)
+        stencil_march<N, G, NR, false, false, true, false>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
+      else if (s1)
+        stencil_march<N, G, NR, false, false, false, true>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
+      else
+        stencil_march<N, G, NR, false, CHK_MARCH_DEDUP>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
     } else {
       for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
         const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
