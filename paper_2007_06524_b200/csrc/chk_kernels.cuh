@@ -41,6 +41,15 @@
 #ifndef CHK_MID_RPF
 #define CHK_MID_RPF 1
 #endif
+#ifndef CHK_FUSED_PF  // n = 512 middle pass: L2 prefetch of the residual / diagonal tile at the
+#define CHK_FUSED_PF 1  // start of each realization
+#endif
+#ifndef CHK_FUSED_QPF  // n = 512 middle pass: L2 prefetch of the Q' rows of the CTA one wave ahead
+#define CHK_FUSED_QPF 0
+#endif
+#ifndef CHK_FUSED_AHEAD  // CTAs per wave of the n = 512 middle pass (one 512-thread CTA per SM)
+#define CHK_FUSED_AHEAD 148
+#endif
 #ifndef CHK_SC_FENCE
 #define CHK_SC_FENCE 0
 #endif
@@ -1342,9 +1351,18 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
     mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
   }
   const double scale = 2.0 / ((double)N * N * N);
+  if (CHK_FUSED_PF && DG && threadIdx.x >= 32 && threadIdx.x < 36) {  // diagonal tile -> L2 (first use: fused last stage)
+    constexpr uint32_t q = N * GW * sizeof(double) / 4;
+    bulk_prefetch_l2(reinterpret_cast<const char*>(Dg) + (threadIdx.x - 32) * q, q);
+  }
+  bool ahead_done = false;
   for (int j = 0; j < NB; ++j) {
     if (!s_act[j]) continue;
     const int b = b0 + j;
+    if (CHK_FUSED_PF && MODE == MID_ITER && threadIdx.x < 4) {  // residual tile -> L2 (read in the fused last stage)
+      constexpr uint32_t q = N * GW * sizeof(double2) / 4;
+      bulk_prefetch_l2(reinterpret_cast<const char*>(ctl.Rh + ((size_t)b * TILES + tile) * N * GW) + threadIdx.x * q, q);
+    }
     // ---- load + group combine (registers) -> smem ----
     for (int item = threadIdx.x; item < N * W; item += blockDim.x) {
       const int w = item % W, x0 = item / W;
@@ -1357,6 +1375,26 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
       reg_fft<G, false>(v, pl.tw, N);
 #pragma unroll
       for (int g = 0; g < G; ++g) buf[x0 * RS + g * W + w] = v[g];
+    }
+    if (CHK_FUSED_QPF && !ahead_done) {
+      // Q' rows of the CTA one wave ahead -> L2 while this CTA runs its shared-memory
+      // stages (one CTA per SM: nothing else would overlap the next CTA's loads)
+      ahead_done = true;
+      const int na = blockIdx.x + CHK_FUSED_AHEAD;
+      if (na < (int)gridDim.x) {
+        const int bga = na / TILES, tla = na - bga * TILES;
+        const int c0a = tla * W;
+        for (int ja = 0; ja < NB; ++ja) {
+          const int ba = bga * NB + ja;
+          if (ba >= B || (MODE != MID_APPLY && ctl.st[ba].status != ST_ACTIVE)) continue;
+          for (int item = threadIdx.x; item < N * W; item += blockDim.x) {
+            const int w = item % W, x0 = item / W;
+            const size_t rbase = slab_row(sg, B, G, x0 >> nsh, ba, x0 & (sg.nloc - 1), 0) + (IL ? c0a * G : c0a) + w;
+#pragma unroll
+            for (int g = 0; g < G; ++g) asm volatile("prefetch.global.L2 [%0];" ::"l"(S + rbase + (size_t)g * GSTR));
+          }
+        }
+      }
     }
     __syncthreads();
     FftRecButLast<N, N, false, GW>::run(buf, X0Addr{RS}, pl.tw, 1);
