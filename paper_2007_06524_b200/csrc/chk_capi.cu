@@ -249,6 +249,14 @@ struct Ops {
       const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
       CHK_CUDA(allow_smem(mid_column_r256_kernel<NBX, MODE>, sm));
       mid_column_r256_kernel<NBX, MODE><<<grid, 256, sm, s>>>(S, pl, ctl, sg, it, B);
+#if CHK_R512
+    } else if (N == 512 && CHK_R512) {
+      // register-phase kernel (x0 radix order 2, 8, 2, 8, 2; diagonal from the plan table)
+      if (!pl.D) return fail(CHK_EINVAL, "n = 512 middle pass needs the plan's diagonal table");
+      const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
+      CHK_CUDA(allow_smem(mid_column_r512_kernel<NBX, MODE>, sm));
+      mid_column_r512_kernel<NBX, MODE><<<grid, 512, sm, s>>>(S, pl, ctl, sg, it, B);
+#endif
     } else if (pl.D && mid_dg()) {
       const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
       CHK_CUDA(allow_smem(mid_column_fused_kernel<N, G, W, NBX, MODE, true>, sm));
@@ -579,7 +587,7 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
   // diagonal tiles of every middle-pass tile (n^2 (n/2+1) doubles: 8.5 MB at
   // n = 128, 539 MB at n = 512); CHK_NO_DTILE=1 evaluates them per CTA instead
   // (n = 256 always has the table: its middle pass reads it)
-  if (!(getenv("CHK_NO_DTILE") && atoi(getenv("CHK_NO_DTILE"))) || (n == 256 && CHK_R256)) {
+  if (!(getenv("CHK_NO_DTILE") && atoi(getenv("CHK_NO_DTILE"))) || (n == 256 && CHK_R256) || (n == 512 && CHK_R512)) {
     const int rc2 = plan_dtiles(p);
     if (rc2) {
       chk_precond_plan_destroy(p);

@@ -230,9 +230,17 @@ __device__ __forceinline__ int dig_freq(int p) {
 #ifndef CHK_R256
 #define CHK_R256 1
 #endif
+// n = 512 (CHK_R512=1): 2, 8, 2, 8, 2 -- radix-2 first stage shared with the group
+// combine (mid_column_r512_kernel), then two register-fused radix-16 passes.  Off by
+// default: measured 2105 us vs 2001 us for mid_column_fused on config 5 (128-register
+// cap at 512 threads spills; the scattered 16-byte row loads become MIO-throttled).
+#ifndef CHK_R512
+#define CHK_R512 0
+#endif
 __host__ __device__ constexpr int x0_radix(int N, int M) {
-  return (N == 256 && CHK_R256) ? ((M == 256 || M == 2) ? 2 : 8)
-                                : ((M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2));
+  return (N == 256 && CHK_R256)   ? ((M == 256 || M == 2) ? 2 : 8)
+         : (N == 512 && CHK_R512) ? ((M == 512 || M == 32 || M == 2) ? 2 : 8)
+                                  : ((M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2));
 }
 // frequency held at position p after the forward x0 transform (x0_radix order)
 template <int N>
@@ -1632,6 +1640,211 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
     });
   }
 }
+
+#if CHK_R512
+// ----------------------------------------------------------------------------
+// kernel 2d: register-phase spectral column pass for n = 512 (x0 radix 2, 8, 2, 8, 2)
+// ----------------------------------------------------------------------------
+// CTA (512 threads, one per SM: the 139 KB tile) = NB realizations x one tile (W = 1
+// column x G = 16 groups = 16 slots, 512 x0 positions; contiguous spectrum layout).
+//   A  (thread = x0 row; rows j and j + 256 in lanes l, l ^ 16 of one warp): group
+//      combine in registers + the radix-2 x0 stage (M = 512) by shuffle   -> smem
+//   B1 (thread = slot, 256-block, offset j0 < 16): radix-8 stage M = 256 and radix-2
+//      stage M = 32 in registers (16 positions j0 + 16 m)               smem -> smem
+//   B2 (thread = slot, 16-block): radix-8 (M = 16) + radix-2 (M = 2), residual
+//      update / diagonal (plan table) / Parseval, inverse                 smem -> smem
+//   B1' inverse M = 32 + M = 256 stages;  A' inverse radix-2 + group combine -> HBM
+// Fusing consecutive DIF stages in registers does the same arithmetic in the same
+// order as separate stages.  8 shared-memory passes per element (mid_column_fused: 12).
+#ifndef CHK_R512_RPF
+#define CHK_R512_RPF 1
+#endif
+template <int NB, int MODE>
+__global__ void __launch_bounds__(512, 1) mid_column_r512_kernel(double2* __restrict__ S, PlanDev pl, SolveCtl ctl,
+                                                                 SlabGeo sg, int it, int B) {
+  constexpr int N = 512, G = 16, W = 1, GW = G * W, RS = GW + 1;
+  static_assert(IlW<N>::value == 0, "contiguous spectrum layout expected at n = 512");
+  static_assert(x0_radix(N, 512) == 2 && x0_radix(N, 256) == 8 && x0_radix(N, 32) == 2 && x0_radix(N, 16) == 8 &&
+                    x0_radix(N, 2) == 2,
+                "x0 radix order 2, 8, 2, 8, 2");
+  const int TILES = sg.tiles;
+  const int nsh = __ffs(sg.nloc) - 1;
+  const size_t GSTR = (size_t)sg.ncols;
+  extern __shared__ double2 buf[];  // [N][RS]
+  __shared__ double scratch[64];
+  __shared__ int s_k1[GW], s_k2[GW];
+  __shared__ double s_wgt[GW];
+  __shared__ double2 s_tw[GW];
+  __shared__ int s_act[NB];
+  __shared__ double s_alpha[NB];
+  __shared__ double s_wsum[NB * 16 * 2];
+  __shared__ int s_dc;
+  const int bg = blockIdx.x / TILES;
+  const int tile = blockIdx.x - bg * TILES;
+  const int c0 = tile * W;
+  const int cg0 = (sg.tile_off + tile) * W;
+  const int b0 = bg * NB;
+  if (threadIdx.x == 0) {
+    int any = 0;
+    for (int j = 0; j < NB; ++j) {
+      const int b = b0 + j;
+      int a = (b < B);
+      if (a && MODE != MID_APPLY) a = (ctl.st[b].status == ST_ACTIVE);
+      s_act[j] = a;
+      s_alpha[j] = (a && MODE == MID_ITER) ? ctl.st[b].alpha : 0.0;
+      any |= a;
+    }
+    scratch[0] = any;
+    s_dc = -1;
+  }
+  __syncthreads();
+  if (scratch[0] == 0.0) return;
+  mid_slots<N, G, W>(cg0, pl, s_k1, s_k2, s_wgt, s_tw);
+  __syncthreads();
+  if (MODE != MID_APPLY && threadIdx.x < GW && s_k1[threadIdx.x] == 0 && s_k2[threadIdx.x] == 0)
+    s_dc = threadIdx.x;
+  __syncthreads();
+  const double* Dg = pl.D + (size_t)(cg0 / W) * N * GW;
+  if (CHK_R512_RPF && threadIdx.x >= 32 && threadIdx.x < 36) {  // diagonal tile -> L2 (read in B2)
+    constexpr uint32_t q = N * GW * sizeof(double) / 4;
+    bulk_prefetch_l2(reinterpret_cast<const char*>(Dg) + (threadIdx.x - 32) * q, q);
+  }
+  const double scale = 2.0 / ((double)N * N * N);
+  // phase A item: x0 pair jA, jA + 256 in lanes l and l ^ 16 of one warp (row x0A = jA + 256 hA)
+  const int hA = (threadIdx.x >> 4) & 1, jA = (threadIdx.x >> 5) * 16 + (threadIdx.x & 15);
+  const int x0A = jA + 256 * hA;
+  for (int j = 0; j < NB; ++j) {
+    if (!s_act[j]) continue;
+    const int b = b0 + j;
+    if (CHK_R512_RPF && MODE == MID_ITER && threadIdx.x < 4) {  // residual tile -> L2 before B2 reads it
+      constexpr uint32_t q = N * GW * sizeof(double2) / 4;
+      bulk_prefetch_l2(reinterpret_cast<const char*>(ctl.Rh + ((size_t)b * TILES + tile) * N * GW) + threadIdx.x * q, q);
+    }
+    // ---- A: loads, group combine, radix-2 stage (M = 512; partner row by shuffle) ----
+    {
+      double2 v[G];
+      const size_t rbase = slab_row(sg, B, G, x0A >> nsh, b, x0A & (sg.nloc - 1), 0) + c0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) v[g] = S[rbase + (size_t)g * GSTR];
+#pragma unroll
+      for (int g = 1; g < G; ++g) v[g] = cmul(v[g], s_tw[g]);
+      reg_fft<G, false>(v, pl.tw, N);
+      const double2 t1 = __ldg(pl.tw + jA);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double2 o = make_double2(__shfl_xor_sync(0xffffffffu, v[g].x, 16), __shfl_xor_sync(0xffffffffu, v[g].y, 16));
+        buf[x0A * RS + g] = hA ? cmul(csub(o, v[g]), t1) : cadd(v[g], o);
+      }
+    }
+    __syncthreads();
+    // ---- B1: radix-8 stage M = 256 (stride 32) + radix-2 stage M = 32 (stride 16) ----
+    const int sB = threadIdx.x % GW, j0 = (threadIdx.x / GW) % 16, blkB = threadIdx.x / (16 * GW);
+    double2* baseB = buf + (blkB * 256 + j0) * RS + sB;  // position blk*256 + j0 + 16 (c + 2 t) -> v[c][t]
+    {
+      double2 v[2][8];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[c][t] = baseB[(16 * c + 32 * t) * RS];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        dftR<8, false>(v[c]);
+        const int jj = j0 + 16 * c;
+        if (jj > 0) {
+#pragma unroll
+          for (int m = 1; m < 8; ++m) v[c][m] = cmul(v[c][m], __ldg(pl.tw + jj * m * 2));
+        }
+      }
+      const double2 t2 = __ldg(pl.tw + j0 * 16);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const double2 a = cadd(v[0][t], v[1][t]);
+        const double2 d = csub(v[0][t], v[1][t]);
+        baseB[(32 * t) * RS] = a;
+        baseB[(16 + 32 * t) * RS] = j0 > 0 ? cmul(d, t2) : d;
+      }
+    }
+    __syncthreads();
+    // ---- B2: last two stages, residual / diagonal / Parseval, first two inverse stages ----
+    double rr = 0.0, rz = 0.0;
+    {
+      const int s = threadIdx.x % GW, blk = threadIdx.x / GW;  // 32 blocks of 16 positions
+      double2* row = buf + (blk * 16) * RS + s;
+      double2 v[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = row[e * RS];
+      reg_fft<16, false>(v, pl.tw, N);
+      double2* Rt = ctl.Rh + ((size_t)b * TILES + tile) * N * GW + (blk * 16) * GW + s;
+      const double wgt = s_wgt[s];
+      const double al = s_alpha[j];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int pos0 = blk * 16 + e;
+        // mean projection of z (solver.py:153,179): the zero-frequency coefficient is 0
+        const double D = (pos0 == 0 && s == s_dc) ? 0.0 : __ldg(Dg + pos0 * GW + s);
+        v[e] = mid_point<MODE>(v[e], D, wgt, scale, al, Rt + e * GW, rr, rz);
+      }
+      reg_fft<16, true>(v, pl.tw, N);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) row[e * RS] = v[e];
+    }
+    __syncthreads();
+    // ---- B1': inverse M = 32 stage, inverse M = 256 stage ----
+    {
+      double2 v[2][8];
+      const double2 t2 = __ldg(pl.tw + j0 * 16);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const double2 a = baseB[(32 * t) * RS];
+        const double2 d0 = baseB[(16 + 32 * t) * RS];
+        const double2 d = j0 > 0 ? cmulc(d0, t2) : d0;
+        v[0][t] = cadd(a, d);
+        v[1][t] = csub(a, d);
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int jj = j0 + 16 * c;
+        if (jj > 0) {
+#pragma unroll
+          for (int m = 1; m < 8; ++m) v[c][m] = cmulc(v[c][m], __ldg(pl.tw + jj * m * 2));
+        }
+        dftR<8, true>(v[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) baseB[(16 * c + 32 * t) * RS] = v[c][t];
+    }
+    __syncthreads();
+    // ---- A': inverse radix-2 stage (partner row by shuffle), inverse group combine, store ----
+    {
+      double2 v[G];
+      const double2 t1 = __ldg(pl.tw + jA);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double2 x = hA ? cmulc(buf[x0A * RS + g], t1) : buf[x0A * RS + g];
+        const double2 o = make_double2(__shfl_xor_sync(0xffffffffu, x.x, 16), __shfl_xor_sync(0xffffffffu, x.y, 16));
+        v[g] = hA ? csub(o, x) : cadd(x, o);
+      }
+      reg_fft<G, true>(v, pl.tw, N);
+#pragma unroll
+      for (int g = 1; g < G; ++g) v[g] = cmulc(v[g], s_tw[g]);
+      const size_t rbase = slab_row(sg, B, G, x0A >> nsh, b, x0A & (sg.nloc - 1), 0) + c0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) S[rbase + (size_t)g * GSTR] = v[g];
+    }
+    if (MODE != MID_APPLY) warp_partials(rr, rz, s_wsum, j);
+    __syncthreads();
+  }
+  if (MODE != MID_APPLY) {
+    const double inv = 1.0 / ((double)N * N * N);  // Parseval: (1/N^3) sum conj(X) Y
+    mid_tickets<NB>(s_wsum, s_act, b0, tile, TILES, ctl, scratch, [&](int b, double t0, double t1) {
+      mid_decide(ctl.st + b, ctl, b, it, t0 * inv, t1 * inv);
+    });
+  }
+}
+
+#endif  // CHK_R512
 
 // ----------------------------------------------------------------------------
 // kernel 2b: register-resident spectral column pass (n <= 128)
