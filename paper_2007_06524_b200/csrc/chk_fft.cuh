@@ -182,6 +182,100 @@ __device__ __forceinline__ void fft_smem(double2* buf, const Addr& addr,
   if constexpr (N > 1) FftRec<N, N, INV, NP>::run(buf, addr, tw, ntab / N);
 }
 
+// In-register in-place DIF / inverse DIT of length L on v[0..L): identical
+// index semantics to fft_smem<L> (digit-reversed output), all loops unrolled.
+template <int L, int M, bool INV>
+struct RegFft {
+  __device__ __forceinline__ static void run(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
+    constexpr int R = Radix<M>::value, S = M / R;
+    if constexpr (INV && S > 1) RegFft<L, S, true>::run(v, tw, ntab);
+#pragma unroll
+    for (int blk = 0; blk < L / M; ++blk) {
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        double2 a[R];
+#pragma unroll
+        for (int t = 0; t < R; ++t) a[t] = v[blk * M + j + t * S];
+        if constexpr (!INV) {
+          dftR<R, false>(a);
+          if (j > 0) {
+#pragma unroll
+            for (int m = 1; m < R; ++m) a[m] = cmul(a[m], __ldg(tw + (j * m) * (ntab / M)));
+          }
+        } else {
+          if (j > 0) {
+#pragma unroll
+            for (int m = 1; m < R; ++m) a[m] = cmulc(a[m], __ldg(tw + (j * m) * (ntab / M)));
+          }
+          dftR<R, true>(a);
+        }
+#pragma unroll
+        for (int t = 0; t < R; ++t) v[blk * M + j + t * S] = a[t];
+      }
+    }
+    if constexpr (!INV && S > 1) RegFft<L, S, false>::run(v, tw, ntab);
+  }
+};
+template <int L, bool INV>
+__device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
+  if constexpr (L > 1) RegFft<L, L, INV>::run(v, tw, ntab);
+}
+
+// Stages of a length-N transform down to (forward) / up from (inverse) sub-length
+// BL, the block of the last two stages; FftStop<N, N, INV, NP, BL> runs them in smem.
+template <int M>
+struct LastTwo {  // sub-length at which the last two stages start
+  static constexpr int R = Radix<M>::value;
+  static constexpr int value = ((M / R) > 1 && (M / R) / Radix<M / R>::value > 1) ? LastTwo<M / R>::value : M;
+};
+template <>
+struct LastTwo<1> {
+  static constexpr int value = 1;
+};
+template <int N, int M, bool INV, int NP, int BL>
+struct FftStop {
+  template <class Addr>
+  __device__ __forceinline__ static void run(double2* buf, const Addr& addr, const double2* __restrict__ tw, int twstride) {
+    if constexpr (M > BL) {
+      constexpr int R = Radix<M>::value;
+      if constexpr (!INV) {
+        fft_stage<N, M, false, NP>(buf, addr, tw, twstride);
+        __syncthreads();
+        FftStop<N, M / R, false, NP, BL>::run(buf, addr, tw, twstride);
+      } else {
+        FftStop<N, M / R, true, NP, BL>::run(buf, addr, tw, twstride);
+        fft_stage<N, M, true, NP>(buf, addr, tw, twstride);
+        __syncthreads();
+      }
+    }
+  }
+};
+// fft_smem with the last two stages (a contiguous block of BL elements per pencil)
+// fused in registers when FUSE: same arithmetic in the same order, one shared-memory
+// pass and one barrier fewer.  Same contract as fft_smem (sync before; returns synced).
+template <int N, bool INV, int NP, bool FUSE, class Addr>
+__device__ __forceinline__ void fft_smem_rows(double2* buf, const Addr& addr, const double2* __restrict__ tw,
+                                              int ntab) {
+  if constexpr (!FUSE) {
+    fft_smem<N, INV, NP>(buf, addr, tw, ntab);
+  } else {
+    constexpr int BL = LastTwo<N>::value;
+    static_assert(BL > 1 && BL <= 16, "register block of the last two stages");
+    if constexpr (!INV) FftStop<N, N, false, NP, BL>::run(buf, addr, tw, ntab / N);
+    for (int item = threadIdx.x; item < NP * (N / BL); item += blockDim.x) {
+      const int p = item % NP, blk = item / NP;
+      double2 v[BL];
+#pragma unroll
+      for (int e = 0; e < BL; ++e) v[e] = buf[addr(p, blk * BL + e)];
+      RegFft<BL, BL, INV>::run(v, tw, ntab);  // twiddle (j m) ntab / M as in fft_stage
+#pragma unroll
+      for (int e = 0; e < BL; ++e) buf[addr(p, blk * BL + e)] = v[e];
+    }
+    __syncthreads();
+    if constexpr (INV) FftStop<N, N, true, NP, BL>::run(buf, addr, tw, ntab / N);
+  }
+}
+
 // ----------------------------------------------------------------------------
 // reductions (deterministic: fixed shuffle tree, fixed warp order)
 // ----------------------------------------------------------------------------

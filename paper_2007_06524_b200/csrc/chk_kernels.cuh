@@ -38,6 +38,9 @@
 #ifndef CHK_MARCH_DEDUP  // cell-row de-duplication inside the plane passes' marching stencil
 #define CHK_MARCH_DEDUP 0
 #endif
+#ifndef CHK_FUSE2  // n = 256 plane passes: last two x2 FFT stages (radix 8 x 2) fused in registers;
+#define CHK_FUSE2 0  // off: spills under the 80-register / 3-CTA bound (config 4 fwd +1 %, inv +7 %)
+#endif
 #ifndef CHK_MID_RPF
 #define CHK_MID_RPF 1
 #endif
@@ -989,7 +992,7 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   __syncthreads();
   if (MODE == FWD_Q && (ctl.dbg & 1)) return;  // debug: skip the transform phase
   // R2C along x2: rows of N reals viewed as N/2 complex (z_m = x_2m + i x_2m+1)
-  fft_smem<N2, false, NR>(buf, RowAddr{HP}, pl.tw, N);
+  fft_smem_rows<N2, false, NR, (N == 256 && CHK_FUSE2)>(buf, RowAddr{HP}, pl.tw, N);
   r2c_post<N>(buf, NR, HP, pl.tw);
   __syncthreads();
   // C2C along the x1 group (length NR)
@@ -1255,44 +1258,6 @@ __device__ __forceinline__ double2 mid_point(double2 v, double D, double wgt, do
   return cscale(R, D * scale);
 }
 
-// In-register in-place DIF / inverse DIT of length L on v[0..L): identical
-// index semantics to fft_smem<L> (digit-reversed output), all loops unrolled.
-template <int L, int M, bool INV>
-struct RegFft {
-  __device__ __forceinline__ static void run(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
-    constexpr int R = Radix<M>::value, S = M / R;
-    if constexpr (INV && S > 1) RegFft<L, S, true>::run(v, tw, ntab);
-#pragma unroll
-    for (int blk = 0; blk < L / M; ++blk) {
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        double2 a[R];
-#pragma unroll
-        for (int t = 0; t < R; ++t) a[t] = v[blk * M + j + t * S];
-        if constexpr (!INV) {
-          dftR<R, false>(a);
-          if (j > 0) {
-#pragma unroll
-            for (int m = 1; m < R; ++m) a[m] = cmul(a[m], __ldg(tw + (j * m) * (ntab / M)));
-          }
-        } else {
-          if (j > 0) {
-#pragma unroll
-            for (int m = 1; m < R; ++m) a[m] = cmulc(a[m], __ldg(tw + (j * m) * (ntab / M)));
-          }
-          dftR<R, true>(a);
-        }
-#pragma unroll
-        for (int t = 0; t < R; ++t) v[blk * M + j + t * S] = a[t];
-      }
-    }
-    if constexpr (!INV && S > 1) RegFft<L, S, false>::run(v, tw, ntab);
-  }
-};
-template <int L, bool INV>
-__device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
-  if constexpr (L > 1) RegFft<L, L, INV>::run(v, tw, ntab);
-}
 
 // Fused shared-memory kernel for large n (n >= 256: the plane slab forces G >= 8):
 // load + group combine in registers, the x0 stages but the last through shared
@@ -2283,7 +2248,7 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     fft_smem<NR, true, H>(buf, ColAddr{HP}, pl.tw, N);
     c2r_pre<N>(buf, NR, HP, pl.tw);
     __syncthreads();
-    fft_smem<N2, true, NR>(buf, RowAddr{HP}, pl.tw, N);
+    fft_smem_rows<N2, true, NR, (N == 256 && CHK_FUSE2)>(buf, RowAddr{HP}, pl.tw, N);
   }
   const double* sm = reinterpret_cast<const double*>(buf);
   constexpr int Q4 = N / 4;
