@@ -12,7 +12,9 @@ value  = DOF-iterations/s over all ranks (sum n^3 * iterations / max-over-ranks
          device time of K steps).  Realizations/s is reported beside it.
 e2e    = the same metric through the reference-facing call with HOST buffers:
          H2D of beta + f from pinned memory, the solve, D2H of u + reports.
-Multi-GPU (torchrun): realization sharding, weak scaling, no data-path collective.
+Multi-GPU: `--gpus N` starts N ranks itself (or run it under torchrun); the
+configured batch is sharded 256/N per GPU by global realization index (strong
+scaling, no data-path collective); config 5 runs slab-decomposed.
 --impl reference: the reference algorithm on host cores (the CPU oracle port,
 oracle/checkerhom_oracle.py -- the reference is pure Python and cannot be
 compiled or shipped), process pool over all host threads, bounded sample.
@@ -130,65 +132,149 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_inputs(chk, orc_free_cfg, cfg_id, rank, per_rank, torch):
-    """Seeded synthetic realizations m = rank*per_rank + j (reference generator)."""
+def config_dict(cfg_id, world, slab=False):
+    """The `config` object of the JSON line -- identical for our arm and the
+    reference arm at the same N."""
     c = CFG[cfg_id]
-    lat = chk.LatticeConfig(d=3, L=c["L"], n0=c["n0"], alpha="1/2", lam=c["lam"])
-    ms = [rank * per_rank + j for j in range(per_rank)]
-    seeds = [chk.derive_seed(0, m) for m in ms]
-    beta = np.stack([chk.sample_realization(lat, s).beta_cells.ravel() for s in seeds])
-    A = chk.StiffnessBatch(lat, beta)
-    if c["rhs"] == "corrector":
-        F = chk.corrector_rhs_batched(A, 1)
+    n = c["n0"] * c["L"]
+    d = {"workload": f"config{cfg_id}: {CONFIG_NAMES[cfg_id]}", "n": n, "realizations": c["batch"],
+         "preconditioner": "lkr eps_rank=1e-8", "tol": c["tol"],
+         "l2": "inputs 8*n^3*B bytes per vector >> 126 MB L2 (no flush needed)"}
+    if slab:
+        d["parallelism"] = f"slab x{world} (x0 planes; NCCL halo + all_to_all + allreduce)"
     else:
-        n = lat.n
-        F = torch.empty((per_rank, n ** 3), dtype=torch.float64, device="cuda")
-        for j, s in enumerate(seeds):
-            f = np.random.default_rng(s).standard_normal(n ** 3)
-            F[j].copy_(torch.from_numpy(f - f.mean()))
-    return lat, beta, A, F
+        d["parallelism"] = f"realization sharding x{world} (contiguous global-index blocks, no collective)"
+    return d
+
+
+def launch_ranks(args):
+    """`python bench.py --gpus N` without torchrun: start N ranks (one process per
+    GPU, 127.0.0.1 rendezvous) running this same command; rank 0 prints the line."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+class Dist:
+    """Rank bookkeeping + the few collectives the bench needs (barrier, max/sum of
+    a float vector); backend nccl on GPUs, gloo for the CPU dry run."""
+
+    def __init__(self, backend):
+        import torch
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = backend
+        self.dev = None
+        if backend == "nccl":
+            torch.cuda.set_device(self.local if self.world > 1 else 0)
+            self.dev = torch.device("cuda", torch.cuda.current_device())
+        if self.world > 1:
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group("gloo")
+
+    def barrier(self):
+        import torch
+
+        if self.world > 1:
+            self.dist.barrier()
+        if self.backend == "nccl":
+            torch.cuda.synchronize()
+
+    def reduce(self, vals, op):
+        import torch
+
+        t = torch.tensor(vals, dtype=torch.float64, device=self.dev if self.backend == "nccl" else "cpu")
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return [float(v) for v in t.cpu()]
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def run_dry(args):
+    """CPU dry run of the multi-rank harness (gloo): the launcher, the sharding of
+    the configured batch by global index, and the max-over-ranks reduction, with
+    the GPU solve replaced by a stub that reports a fixed iteration count."""
+    from paper_2007_06524_b200.lattice import derive_seed
+    from paper_2007_06524_b200.sharding import shard_range
+
+    D = Dist("gloo")
+    c = CFG[args.config]
+    n = c["n0"] * c["L"]
+    lo, hi = shard_range(c["batch"], D.rank, D.world)
+    seeds = [derive_seed(0, m) for m in range(lo, hi)]
+    D.barrier()
+    t0 = time.perf_counter()
+    its = 40 * len(seeds) * args.steps  # stub: 40 iterations per realization
+    dt = time.perf_counter() - t0 + 1e-3
+    D.barrier()
+    mx = D.reduce([dt], "max")
+    tot = D.reduce([float(its) * n ** 3, float(len(seeds) * args.steps)], "sum")
+    per_rank = D.reduce([float(len(seeds)) if r == D.rank else 0.0 for r in range(D.world)], "sum")
+    if D.rank == 0:
+        print(json.dumps({"metric": METRIC, "value": tot[0] / mx[0], "unit": UNIT, "n_gpus": D.world,
+                          "steps": args.steps, "warmup": args.warmup, "scaling": "strong", "dry_run": True,
+                          "realizations_per_rank": [int(v) for v in per_rank],
+                          "first_seed_index_per_rank": [shard_range(c["batch"], r, D.world)[0]
+                                                        for r in range(D.world)],
+                          "config": config_dict(args.config, D.world)}), flush=True)
+    D.close()
 
 
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     import paper_2007_06524_b200 as chk
     from paper_2007_06524_b200 import _lib
+    from paper_2007_06524_b200.sharding import shard_range
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
+    D = Dist("nccl")
+    world, rank, dev = D.world, D.rank, D.dev
     cfg_id = args.config
     c = CFG[cfg_id]
-    per_rank = c["batch"]  # weak scaling: every rank solves one full config batch
-    lat, beta_np, A, F = make_inputs(chk, None, cfg_id, rank, per_rank, torch)
+    # strong scaling: the configured batch (config 3: 256 realizations) is split
+    # into contiguous global-index blocks, 256/N per GPU (sharding.shard_range)
+    lo, hi = shard_range(c["batch"], rank, world)
+    per_rank = hi - lo
+    lat = chk.LatticeConfig(d=3, L=c["L"], n0=c["n0"], alpha="1/2", lam=c["lam"])
     n = lat.n
     nb = n ** 3
+    seeds = [chk.derive_seed(0, m) for m in range(lo, hi)]
+    beta = chk.sample_cells_device(lat, seeds)  # bit-identical to sample_realization
+    A = chk.StiffnessBatch(lat, beta)
+    f_gauss = None
+    if c["rhs"] == "corrector":
+        F = chk.corrector_rhs_batched(A, 1)
+    else:
+        f_gauss = np.stack([np.random.default_rng(s).standard_normal(nb) for s in seeds])
+        f_gauss -= f_gauss.mean(axis=1, keepdims=True)
+        F = torch.from_numpy(f_gauss).to(dev)
     opts = chk.SolveOptions(tol=c["tol"], preconditioner="lkr", eps_rank=1e-8)
     P = chk.make_preconditioner(3, n, opts)
     U = torch.empty_like(F)
     ws = chk.solver.Workspace()
     lib = _lib.load()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
     def one_step():
-        res = chk.pcg_solve_batched(A, F, opts, P, out=U, record_history=False, workspace=ws)
-        return res
+        return chk.pcg_solve_batched(A, F, opts, P, out=U, record_history=False, workspace=ws)
 
     for _ in range(args.warmup):
         res = one_step()
-    barrier()
+    D.barrier()
     clocks = ClockSampler(dev.index)
     clocks.start()
     lib.chk_profile_enable(1)
@@ -198,17 +284,16 @@ def run_ours(args):
     dof_its = 0
     launches = 0
     reals = 0
-    barrier()
+    D.barrier()
     ev0.record(stream)
     for _ in range(args.steps):
         res = one_step()
         dof_its += int(np.sum(res.iterations)) * nb
         launches += res.launches
         reals += per_rank
-        if not os.environ.get("CHK_DEBUG_FLAGS"):
-            assert np.all(res.status == 0), "a realization did not converge"
+        assert np.all(res.status == 0), "a realization did not converge"
     ev1.record(stream)
-    barrier()
+    D.barrier()
     clk = clocks.stop()
     ms = float(ev0.elapsed_time(ev1))
     prof_ms = np.zeros(5, dtype=np.float64)
@@ -220,46 +305,38 @@ def run_ours(args):
     # for the matvec and the preconditioner apply at n >= 128), same batch ------
     standalone = standalone_ops(lib, A, F, U, P, args.steps, torch)
 
-    # --- e2e: reference-facing call with host buffers --------------------------
-    # chk_pcg_solve_host: pinned numpy-side inputs/outputs, the batch streamed
-    # through the GPU in 4 chunks with H2D / D2H overlapped with the solves
-    beta_h = torch.from_numpy(beta_np).pin_memory()
-    F_h = F.cpu().pin_memory()
-    U_h = torch.empty_like(F_h).pin_memory()
+    # --- e2e: seeds -> host solutions through the public API -----------------
+    # pcg_solve_seeds: host SeedSequence hashes -> Philox keys (H2D) -> cells drawn
+    # on the device -> corrector load on the device -> solve -> u D2H (pinned),
+    # chunked over lanes so copies and convergence tails overlap other chunks
+    U_h = torch.empty((per_rank, nb), dtype=torch.float64).pin_memory()
+    f_h = torch.from_numpy(f_gauss).pin_memory() if f_gauss is not None else None
     ws_h = chk.solver.Workspace()
     del U
     ws.buf = None
     torch.cuda.empty_cache()
     e2e_ms = []
     for step in range(args.warmup + args.steps):
-        barrier()
+        D.barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        res_e = chk.pcg_solve_host(lat, beta_h, F_h, opts, P, out=U_h, record_history=False, workspace=ws_h,
-                                   chunk=args.e2e_chunk or None)
+        step_seeds = [chk.derive_seed(0, m) for m in range(lo, hi)]  # the host work of the step
+        res_e = chk.pcg_solve_seeds(lat, step_seeds, opts, P, rhs=f_h if f_h is not None else 1, out=U_h,
+                                    record_history=False, workspace=ws_h, chunk=args.e2e_chunk or None)
         t1.record(stream)
-        barrier()
+        D.barrier()
         if step >= args.warmup:
             e2e_ms.append(float(t0.elapsed_time(t1)))
-    assert np.array_equal(res_e.iterations, res.iterations)
+    assert np.array_equal(res_e.iterations, res.iterations), "e2e iterations differ from the device-resident solve"
     e2e_dof_its = int(np.sum(res_e.iterations)) * nb  # identical inputs every step
-    h2d = beta_h.numel() * 8 + F_h.numel() * 8
+    h2d = per_rank * 16 + (f_h.numel() * 8 if f_h is not None else 0)
     d2h = U_h.numel() * 8 + per_rank * (4 + 8 + 4 + 4)
 
     # --- max over ranks -------------------------------------------------------
-    tot = torch.tensor([ms, float(dof_its), float(reals), float(launches),
-                        float(np.mean(e2e_ms)), float(e2e_dof_its)], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = tot.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm_ = tot.clone()
-        dist.all_reduce(sm_, op=dist.ReduceOp.SUM)
-        ms_max, e2e_max = float(mx[0]), float(mx[4])
-        dof_total, reals_total, launches_total, e2e_dof_total = float(sm_[1]), float(sm_[2]), float(sm_[3]), float(sm_[5])
-    else:
-        ms_max, e2e_max = ms, float(np.mean(e2e_ms))
-        dof_total, reals_total, launches_total, e2e_dof_total = float(dof_its), float(reals), float(launches), float(e2e_dof_its)
+    ms_max, e2e_max = D.reduce([ms, float(np.mean(e2e_ms))], "max")
+    dof_total, reals_total, launches_total, e2e_dof_total, h2d_tot, d2h_tot = D.reduce(
+        [float(dof_its), float(reals), float(launches), float(e2e_dof_its), float(h2d), float(d2h)], "sum")
 
     if rank == 0:
         peak, peak_kind = measured_peaks()
@@ -314,27 +391,30 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference seeded generator: derive_seed(0,m), Philox cells, corrector/Gaussian RHS)",
-            "config": {"workload": f"config{cfg_id}: {CONFIG_NAMES[cfg_id]}", "n": n,
-                       "realizations_per_gpu": per_rank, "preconditioner": "lkr eps_rank=1e-8",
-                       "parallelism": f"realization sharding x{world}",
-                       "l2": "inputs 8*n^3*B bytes per vector >> 126 MB L2 (no flush needed)"},
+            "config": config_dict(cfg_id, world),
+            "realizations_per_gpu": per_rank,
             "realizations_per_s": reals_total / (ms_max / 1e3),
             "dof_iterations": dof_total,
             "roofline": roofline,
             "kernels": per_kernel,
             "e2e": {"value": e2e_dof_total / (e2e_max / 1e3), "unit": UNIT,
-                    "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
-                    "ms_per_step": e2e_max},
+                    "h2d_bytes_per_step": int(h2d_tot), "d2h_bytes_per_step": int(d2h_tot),
+                    "ms_per_step": e2e_max,
+                    "realizations_per_s": c["batch"] / (e2e_max / 1e3),
+                    "path": ("pcg_solve_seeds: seeds -> SeedSequence keys (host) -> Philox cells + corrector "
+                             "load on the device -> solve -> u to pinned host memory"
+                             if f_h is None else
+                             "pcg_solve_seeds with the host Gaussian loads (numpy default_rng, generated "
+                             "before the timed region) uploaded per chunk")},
             "standalone": standalone,
             "gpu_launches": int(launches_total),
             "clocks": clk,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    D.close()
 
 
 def standalone_ops(lib, A, F, Y, P, reps, torch):
@@ -446,9 +526,9 @@ def run_reference(args):
                 rates.append(sum(o[0] * o[1] for o in out) / dt)
     value = float(np.mean(rates))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "impl": "reference", "data": "synthetic (same generator as our arm)",
-            "config": {"workload": f"config{cfg_id}: {CONFIG_NAMES[cfg_id]}", "n": n},
+            "config": config_dict(cfg_id, world, slab=cfg_id == 5 and world > 1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
                              "sample": f"per step {workers} realizations of config{cfg_id} solved to the "
                                        f"reference stop rule, one per process (pattern of "
@@ -535,8 +615,7 @@ def run_slab(args):
             "warmup": args.warmup, "ms_per_step": float(ms) / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference seeded generator)",
-            "config": {"workload": f"config{args.config}: {CONFIG_NAMES[args.config]}", "n": n,
-                       "parallelism": f"slab x{world} (x0 planes; NCCL halo + all_to_all + allreduce)"},
+            "config": config_dict(args.config, world, slab=True),
             "realizations_per_s": c["batch"] * args.steps / (float(ms) / 1e3),
             "roofline": {"bound": "hbm", "kernel": "whole iteration", "unit": "GB/s", "peak": peak * world,
                          "peak_kind": peak_kind, "achieved": round(value * B_ALG / 1e9, 1),
@@ -562,8 +641,16 @@ def main():
                     help="realizations per pipelined chunk of the host-buffer solve (default B/4)")
     ap.add_argument("--slab", action="store_true",
                     help="force the slab-decomposed path (default for config 5 when N > 1)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU (gloo) run of the multi-rank harness with a stub solve (tests)")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if os.environ.get("CHK_DEBUG_FLAGS"):
+        sys.exit("bench.py: CHK_DEBUG_FLAGS is set; refusing to time a run")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     elif args.slab or (args.config == 5 and int(os.environ.get("WORLD_SIZE", "1")) > 1):
         run_slab(args)

@@ -155,6 +155,34 @@ int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, c
                            void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Realizations drawn on the device (sample_realization, lattice.py:284-311).
+ * keys: [B][2] Philox4x64 keys of the realizations' streams, i.e.
+ * SeedSequence(seed).generate_state(2, uint64) of each seed (lattice.py:279-281;
+ * the hash stays on the host).  Cell c (C order) is covered iff the c-th
+ * Generator.random() draw is < coverage_prob; its contrast is beta0
+ * (CHK_CONTRAST_FIXED: the caller passes 1 - lam) or, CHK_CONTRAST_TWO_VALUE,
+ * beta0 / beta1 by the (L^3 + c)-th draw < 1/2.  beta: device [B][L^3] out,
+ * bit-identical to the reference's realization.  (The layered contrast stays on
+ * the host path.)
+ * ------------------------------------------------------------------------- */
+#define CHK_CONTRAST_FIXED 0
+#define CHK_CONTRAST_TWO_VALUE 1
+int32_t chk_sample_cells(const chk_grid* grid, const uint64_t* keys, double coverage_prob, int32_t contrast_kind,
+                         double beta0, double beta1, double* beta, int32_t B, void* stream);
+
+/* Seeds-to-solutions pipeline: chk_pcg_solve_host with the realizations drawn
+ * on the device from HOST keys_host [B][2] (as chk_sample_cells) and the load
+ * either the device corrector RHS along rhs_direction (f_host NULL; the PCG
+ * load of homogenize.py:110) or HOST f_host [B][n^3].  u_host and the reports
+ * out as chk_pcg_solve_host; same workspace (chk_pcg_host_workspace_bytes). */
+int32_t chk_pcg_solve_seeds(const chk_grid* grid, const chk_precond_plan* plan, const uint64_t* keys_host,
+                            double coverage_prob, int32_t contrast_kind, double beta0, double beta1,
+                            const double* f_host, int32_t rhs_direction, double* u_host, int32_t B, int32_t chunk,
+                            const chk_pcg_opts* opts, int32_t* iterations, double* final_rel, int32_t* status,
+                            int32_t* rhs_projected, double* history, void* workspace, size_t workspace_bytes,
+                            void* stream);
+
+/* ---------------------------------------------------------------------------
  * Slab decomposition of one grid over `nranks` GPUs (the
  * realization loop of ensemble_run, homogenize.py:133-182, shards instead).
  * Rank r owns planes x0 in [r n/P, (r+1) n/P) of p, u, f and one chunk of the

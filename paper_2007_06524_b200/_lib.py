@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libchkpcg.so")
 CHK_OK, CHK_EINVAL, CHK_EUNSUPPORTED, CHK_ECUDA = 0, 1, 2, 3
 CHK_CONVERGED, CHK_NOT_CONVERGED, CHK_BREAKDOWN = 0, 1, 2
 PRECOND_KIND = {"fourier": 0, "lkr": 1, "regularized": 2}
+CONTRAST_KIND = {"fixed": 0, "two_value": 1}
 
 
 class ChkGrid(ctypes.Structure):
@@ -56,6 +57,9 @@ SIGNATURES = {
     "chk_pcg_host_workspace_bytes": (_sz, [_gp, _vp, _i32, _i32]),
     "chk_pcg_solve_host": (_i32, [_gp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.POINTER(ChkPcgOpts),
                                   _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "chk_sample_cells": (_i32, [_gp, _vp, _dbl, _i32, _dbl, _dbl, _vp, _i32, _vp]),
+    "chk_pcg_solve_seeds": (_i32, [_gp, _vp, _vp, _dbl, _i32, _dbl, _dbl, _vp, _i32, _vp, _i32, _i32,
+                                   ctypes.POINTER(ChkPcgOpts), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "chk_slab_exchange_elems": (_sz, [_gp, _vp, _i32]),
     "chk_slab_workspace_bytes": (_sz, [_gp, _vp, _vp, _i32, _i32]),
     "chk_slab_phase": (_i32, [_gp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

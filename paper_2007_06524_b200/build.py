@@ -11,7 +11,7 @@ REPO = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libchkpcg.so")
 SOURCES = [os.path.join(SRC, "chk_capi.cu")]
-DEPS = SOURCES + [os.path.join(SRC, f) for f in ("chk_fft.cuh", "chk_kernels.cuh", "chk_tma.cuh", "chk_plane.cuh")] + [
+DEPS = SOURCES + [os.path.join(SRC, f) for f in ("chk_fft.cuh", "chk_kernels.cuh", "chk_tma.cuh", "chk_plane.cuh", "chk_sample.cuh")] + [
     os.path.join(REPO, "include", "chk_pcg.h")]
 
 NVCC_FLAGS = [

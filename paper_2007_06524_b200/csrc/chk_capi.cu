@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <exception>
 #include <string>
 #include <thread>
@@ -18,6 +19,7 @@
 
 #include "../../include/chk_pcg.h"
 #include "chk_kernels.cuh"
+#include "chk_sample.cuh"
 
 using namespace chk;
 
@@ -166,40 +168,32 @@ struct Ops {
   }
   static bool slab_ok(int P) { return P >= 1 && N % P == 0 && (N / P) >= 1 && TILES % P == 0 && P <= 64; }
 
-  // raise the dynamic shared-memory limit once per kernel instantiation and size
+  // raise the dynamic shared-memory limit once per (device, kernel instantiation)
+  // and size -- the attribute is per device
   template <class K>
   static cudaError_t allow_smem(K kernel, size_t bytes) {
     if (bytes <= 48 * 1024) return cudaSuccess;
-    static thread_local std::vector<std::pair<const void*, size_t>> done;
+    struct Done {
+      int dev;
+      const void* key;
+      size_t bytes;
+    };
+    static thread_local std::vector<Done> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
     const void* key = reinterpret_cast<const void*>(kernel);
     for (auto& d : done)
-      if (d.first == key && d.second >= bytes) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e == cudaSuccess) done.push_back({key, bytes});
+      if (d.dev == dev && d.key == key && d.bytes >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.push_back({dev, key, bytes});
     return e;
   }
 
-  // plane-pass launch: 2-CTA clusters where the interleaved layout pairs groups (IlC)
   template <class... KA, class... AA>
   static cudaError_t plaunch(void (*kernel)(KA...), dim3 grid, size_t sm, cudaStream_t s, AA... args) {
-    if constexpr (IlC<N>::value > 1) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = grid;
-      cfg.blockDim = dim3(PlaneNT<N>::value);
-      cfg.dynamicSmemBytes = sm;
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = IlC<N>::value;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      return cudaLaunchKernelEx(&cfg, kernel, args...);
-    } else {
-      kernel<<<grid, PlaneNT<N>::value, sm, s>>>(args...);
-      return cudaSuccess;
-    }
+    kernel<<<grid, PlaneNT<N>::value, sm, s>>>(args...);
+    return cudaSuccess;
   }
   static int fwd(int mode, cudaStream_t s, int B, Geo g, const double* beta, const double* src,
                  double* u, double2* S, PlanDev pl, SolveCtl ctl, int it, SlabGeo sg = whole()) {
@@ -249,14 +243,6 @@ struct Ops {
       const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
       CHK_CUDA(allow_smem(mid_column_r256_kernel<NBX, MODE>, sm));
       mid_column_r256_kernel<NBX, MODE><<<grid, 256, sm, s>>>(S, pl, ctl, sg, it, B);
-#if CHK_R512
-    } else if (N == 512 && CHK_R512) {
-      // register-phase kernel (x0 radix order 2, 8, 2, 8, 2; diagonal from the plan table)
-      if (!pl.D) return fail(CHK_EINVAL, "n = 512 middle pass needs the plan's diagonal table");
-      const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
-      CHK_CUDA(allow_smem(mid_column_r512_kernel<NBX, MODE>, sm));
-      mid_column_r512_kernel<NBX, MODE><<<grid, 512, sm, s>>>(S, pl, ctl, sg, it, B);
-#endif
     } else if (pl.D && mid_dg()) {
       const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
       CHK_CUDA(allow_smem(mid_column_fused_kernel<N, G, W, NBX, MODE, true>, sm));
@@ -311,7 +297,6 @@ struct Ops {
   }
   // paired plane pass (pair_plane_kernel): fa.blocks forward + ia.blocks inverse CTAs
   static int pair(cudaStream_t s, const FwdArgs& fa, const InvArgs& ia, PlanDev pl) {
-    if constexpr (IlC<N>::value > 1) return fail(CHK_EUNSUPPORTED, "paired plane pass with clustered plane CTAs");
     const size_t sm = plane_smem();
     const SlabGeo sg = whole();
     dim3 grid(fa.blocks + ia.blocks), block(PlaneNT<N>::value);
@@ -363,6 +348,19 @@ struct Ops {
     case 256: { using O = Ops<256>; __VA_ARGS__; } break;  \
     case 512: { using O = Ops<512>; __VA_ARGS__; } break;  \
     default: return fail(CHK_EUNSUPPORTED, "unsupported n " + std::to_string(n)); \
+  }
+
+// CHK_DISPATCH for contexts that cannot return (sets rc on an unsupported n)
+#define CHK_DISPATCH_V(n, rc, ...)                         \
+  switch (n) {                                             \
+    case 8:   { using O = Ops<8>;   __VA_ARGS__; } break;  \
+    case 16:  { using O = Ops<16>;  __VA_ARGS__; } break;  \
+    case 32:  { using O = Ops<32>;  __VA_ARGS__; } break;  \
+    case 64:  { using O = Ops<64>;  __VA_ARGS__; } break;  \
+    case 128: { using O = Ops<128>; __VA_ARGS__; } break;  \
+    case 256: { using O = Ops<256>; __VA_ARGS__; } break;  \
+    case 512: { using O = Ops<512>; __VA_ARGS__; } break;  \
+    default: rc = fail(CHK_EUNSUPPORTED, "unsupported n"); \
   }
 
 // Realizations in the first half of a paired solve (0: unpaired).  Pairing pays
@@ -587,7 +585,7 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
   // diagonal tiles of every middle-pass tile (n^2 (n/2+1) doubles: 8.5 MB at
   // n = 128, 539 MB at n = 512); CHK_NO_DTILE=1 evaluates them per CTA instead
   // (n = 256 always has the table: its middle pass reads it)
-  if (!(getenv("CHK_NO_DTILE") && atoi(getenv("CHK_NO_DTILE"))) || (n == 256 && CHK_R256) || (n == 512 && CHK_R512)) {
+  if (!(getenv("CHK_NO_DTILE") && atoi(getenv("CHK_NO_DTILE"))) || (n == 256 && CHK_R256)) {
     const int rc2 = plan_dtiles(p);
     if (rc2) {
       chk_precond_plan_destroy(p);
@@ -627,7 +625,6 @@ int32_t chk_precond_apply(const chk_precond_plan* p, const double* r, double* z,
   double2* S = static_cast<double2*>(workspace);
   PlanDev pl = plan_dev(p);
   SolveCtl ctl{};
-  if (const char* dbg = getenv("CHK_DEBUG_FLAGS")) ctl.dbg = atoi(dbg);
   Geo g{};
   g.n = p->n;
   int rc = CHK_OK;
@@ -651,34 +648,46 @@ int32_t chk_stencil_apply(const chk_grid* grid, const double* beta, const double
   double* part = nullptr;
   unsigned* cnt = nullptr;
   if (xy) {
-    // per-CTA partials + tickets of <x, y>: a per-thread scratch buffer kept across
-    // calls (grown on demand; the tickets are zeroed in stream order every call)
+    // per-CTA partials + tickets of <x, y>: a scratch buffer per (thread, device,
+    // stream) kept across calls (grown on demand; the tickets are zeroed in stream
+    // order every call), so overlapping calls on different streams never share it
     struct Scratch {
       int dev = -1;
+      cudaStream_t stream = nullptr;
       void* p = nullptr;
       size_t cap = 0;
-      ~Scratch() {
-        if (p) cudaFree(p);
+    };
+    struct Scratches {
+      std::vector<Scratch> v;
+      ~Scratches() {
+        for (auto& s : v)
+          if (s.p) cudaFree(s.p);
       }
     };
-    static thread_local Scratch sc;
+    static thread_local Scratches scs;
     int dev = 0;
     CHK_CUDA(cudaGetDevice(&dev));
+    Scratch* sc = nullptr;
+    for (auto& e : scs.v)
+      if (e.dev == dev && e.stream == s) sc = &e;
+    if (!sc) {
+      scs.v.push_back(Scratch{dev, s, nullptr, 0});
+      sc = &scs.v.back();
+    }
     const size_t pb = sizeof(double) * 2 * (size_t)grid->n * 16 * B;  // N*G <= 16 n
     const size_t need = pb + sizeof(unsigned) * B;
-    if (sc.cap < need || sc.dev != dev) {
-      if (sc.p) {
-        CHK_CUDA(cudaStreamSynchronize(s));  // earlier calls on this thread may still use it
-        cudaFree(sc.p);
-        sc.p = nullptr;
-        sc.cap = 0;
+    if (sc->cap < need) {
+      if (sc->p) {
+        CHK_CUDA(cudaStreamSynchronize(s));  // earlier calls on this stream may still use it
+        cudaFree(sc->p);
+        sc->p = nullptr;
+        sc->cap = 0;
       }
-      CHK_CUDA(cudaMalloc(&sc.p, need));
-      sc.cap = need;
-      sc.dev = dev;
+      CHK_CUDA(cudaMalloc(&sc->p, need));
+      sc->cap = need;
     }
-    part = static_cast<double*>(sc.p);
-    cnt = reinterpret_cast<unsigned*>(static_cast<char*>(sc.p) + pb);
+    part = static_cast<double*>(sc->p);
+    cnt = reinterpret_cast<unsigned*>(static_cast<char*>(sc->p) + pb);
     CHK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * B, s));
   }
   CHK_DISPATCH(grid->n, { rc = O::stencil(s, B, g, beta, x, y, xy, part, cnt); });
@@ -722,8 +731,7 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PlanDev pl = plan_dev(plan);
   SolveCtl ctl{w.st, w.Rh, w.part, w.hist, maxblk_of(n), opts->max_iter, opts->tol,
-               opts->precond_residual_stopping ? 1 : 0, 0, nullptr, 0};
-  if (const char* dbg = getenv("CHK_DEBUG_FLAGS")) ctl.dbg = atoi(dbg);
+               opts->precond_residual_stopping ? 1 : 0, nullptr, 0};
   RState* hst_all = g_pinned.get((size_t)2 * B);
   RState* hst = hst_all;
   if (!hst_all) return fail(CHK_ECUDA, "cudaMallocHost failed");
@@ -869,28 +877,47 @@ size_t chk_pcg_host_workspace_bytes(const chk_grid* grid, const chk_precond_plan
   if (!grid || !plan || chunk < 1 || max_iter < 1 || !supported_n(grid->n)) return 0;
   const size_t nb = (size_t)grid->n * grid->n * grid->n;
   const size_t lb = (size_t)grid->L * grid->L * grid->L;
-  const size_t slot = align_up(sizeof(double) * (2 * nb + lb) * chunk);
+  const size_t slot = align_up(sizeof(double) * (2 * nb + lb) * chunk) + align_up(2 * sizeof(uint64_t) * chunk);
   const size_t sw = chk_pcg_workspace_bytes(grid, plan, chunk, max_iter);
   if (sw == 0) return 0;
   return (size_t)host_lanes(1 << 30) * (slot + align_up(sw));
 }
 
-int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, const double* beta_host,
-                           const double* f_host, double* u_host, int32_t B, int32_t chunk,
-                           const chk_pcg_opts* opts, int32_t* iterations, double* final_rel,
-                           int32_t* status, int32_t* rhs_projected, double* history,
-                           void* workspace, size_t workspace_bytes, void* stream) {
-  if (!grid || !plan || !beta_host || !f_host || !u_host || B < 1 || chunk < 1 || !opts)
-    return fail(CHK_EINVAL, "bad arguments");
+}  // extern "C"
+
+namespace {
+
+// Inputs of one host pipeline run: per-cell contrasts from host arrays or drawn
+// on the device from Philox keys; the load from a host array or the device
+// corrector kernel.
+struct PipeIn {
+  const double* beta_host;  // [B][L^3] or null (then keys_host)
+  const uint64_t* keys_host;  // [B][2] Philox keys (SeedSequence(seed).generate_state(2, uint64))
+  double cov_p;
+  int ckind;
+  double beta0, beta1;
+  const double* f_host;  // [B][n^3] or null (then the corrector load along rhs_dir)
+  int rhs_dir;
+};
+
+int host_pipeline(const chk_grid* grid, const chk_precond_plan* plan, const PipeIn& in, double* u_host, int B,
+                  int chunk, const chk_pcg_opts* opts, int32_t* iterations, double* final_rel, int32_t* status,
+                  int32_t* rhs_projected, double* history, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!grid || !plan || !u_host || B < 1 || chunk < 1 || !opts) return fail(CHK_EINVAL, "bad arguments");
   if (chunk > B) chunk = B;
+  Geo geo;
+  int rc0 = check_grid(grid, &geo);
+  if (rc0) return rc0;
   const size_t need = chk_pcg_host_workspace_bytes(grid, plan, chunk, opts->max_iter);
   if (!workspace || workspace_bytes < need || need == 0) return fail(CHK_EINVAL, "workspace too small");
   const size_t nb = (size_t)grid->n * grid->n * grid->n;
   const size_t lb = (size_t)grid->L * grid->L * grid->L;
-  const size_t slot_bytes = align_up(sizeof(double) * (2 * nb + lb) * chunk);
+  const size_t data_bytes = align_up(sizeof(double) * (2 * nb + lb) * chunk);
+  const size_t slot_bytes = data_bytes + align_up(2 * sizeof(uint64_t) * chunk);
   const size_t solver_bytes = align_up(chk_pcg_workspace_bytes(grid, plan, chunk, opts->max_iter));
   const int nchunks = (B + chunk - 1) / chunk;
   const int lanes = host_lanes(nchunks);
+  const double h = 1.0 / grid->n;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = 0;
   CHK_CUDA(cudaGetDevice(&dev));
@@ -918,14 +945,46 @@ int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, c
     double* d_f = reinterpret_cast<double*>(base);
     double* d_u = d_f + nb * chunk;
     double* d_b = d_u + nb * chunk;
+    uint64_t* d_k = reinterpret_cast<uint64_t*>(base + data_bytes);
     void* solver_ws = base + slot_bytes;
     if ((e = cudaStreamWaitEvent(ls, start, 0)) != cudaSuccess) bad(CHK_ECUDA, "lane wait", e);
     for (int c = lane; c < nchunks && o.rc == CHK_OK; c += lanes) {
       const int b0 = c * chunk, nbc = (B - b0 < chunk) ? B - b0 : chunk;
-      if ((e = cudaMemcpyAsync(d_b, beta_host + lb * b0, sizeof(double) * lb * nbc, cudaMemcpyHostToDevice, ls)) ||
-          (e = cudaMemcpyAsync(d_f, f_host + nb * b0, sizeof(double) * nb * nbc, cudaMemcpyHostToDevice, ls))) {
-        bad(CHK_ECUDA, "upload", e);
-        break;
+      if (in.beta_host) {
+        if ((e = cudaMemcpyAsync(d_b, in.beta_host + lb * b0, sizeof(double) * lb * nbc, cudaMemcpyHostToDevice, ls))) {
+          bad(CHK_ECUDA, "upload beta", e);
+          break;
+        }
+      } else {
+        if ((e = cudaMemcpyAsync(d_k, in.keys_host + 2 * (size_t)b0, 2 * sizeof(uint64_t) * nbc,
+                                 cudaMemcpyHostToDevice, ls))) {
+          bad(CHK_ECUDA, "upload keys", e);
+          break;
+        }
+        const int ncell = (int)lb;
+        const int gx = (int)std::min<long long>(((long long)ncell / 4 + 255) / 256 + 1, 1184);
+        sample_cells_kernel<<<dim3(gx, nbc), 256, 0, ls>>>(d_k, ncell, in.cov_p, in.ckind, in.beta0, in.beta1, d_b);
+        ++o.launches;
+        if ((e = cudaGetLastError())) {
+          bad(CHK_ECUDA, "sample_cells launch", e);
+          break;
+        }
+      }
+      if (in.f_host) {
+        if ((e = cudaMemcpyAsync(d_f, in.f_host + nb * b0, sizeof(double) * nb * nbc, cudaMemcpyHostToDevice, ls))) {
+          bad(CHK_ECUDA, "upload f", e);
+          break;
+        }
+      } else {
+        // PCG load h^(d-1) * h^(2-d) * 1/2 (c[x+e_i] - c[x-e_i])  (homogenize.py:85-89,110)
+        int rc = CHK_OK;
+        CHK_DISPATCH_V(grid->n, rc, { rc = O::rhs(ls, nbc, geo, d_b, d_f, in.rhs_dir - 1, h * h * (1.0 / h)); });
+        ++o.launches;
+        if (rc) {
+          o.rc = rc;
+          o.err = g_err;
+          break;
+        }
       }
       const int rc = chk_pcg_solve_batched(grid, plan, d_b, d_f, d_u, nbc, opts, iterations ? iterations + b0 : nullptr,
                                            final_rel ? final_rel + b0 : nullptr, status ? status + b0 : nullptr,
@@ -979,6 +1038,53 @@ int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, c
   }
   g_launches = launches;
   return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t chk_pcg_solve_host(const chk_grid* grid, const chk_precond_plan* plan, const double* beta_host,
+                           const double* f_host, double* u_host, int32_t B, int32_t chunk,
+                           const chk_pcg_opts* opts, int32_t* iterations, double* final_rel,
+                           int32_t* status, int32_t* rhs_projected, double* history,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (!beta_host || !f_host) return fail(CHK_EINVAL, "bad arguments");
+  PipeIn in{beta_host, nullptr, 0.0, 0, 0.0, 0.0, f_host, 0};
+  return host_pipeline(grid, plan, in, u_host, B, chunk, opts, iterations, final_rel, status, rhs_projected,
+                       history, workspace, workspace_bytes, stream);
+}
+
+int32_t chk_pcg_solve_seeds(const chk_grid* grid, const chk_precond_plan* plan, const uint64_t* keys_host,
+                            double coverage_prob, int32_t contrast_kind, double beta0, double beta1,
+                            const double* f_host, int32_t rhs_direction, double* u_host, int32_t B, int32_t chunk,
+                            const chk_pcg_opts* opts, int32_t* iterations, double* final_rel, int32_t* status,
+                            int32_t* rhs_projected, double* history, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  if (!keys_host) return fail(CHK_EINVAL, "keys_host is NULL");
+  if (contrast_kind != CHK_CONTRAST_FIXED && contrast_kind != CHK_CONTRAST_TWO_VALUE)
+    return fail(CHK_EINVAL, "contrast_kind must be CHK_CONTRAST_FIXED or CHK_CONTRAST_TWO_VALUE");
+  if (!f_host && (rhs_direction < 1 || rhs_direction > 3))
+    return fail(CHK_EINVAL, "rhs_direction must be in 1..3 when f_host is NULL");
+  PipeIn in{nullptr, keys_host, coverage_prob, contrast_kind, beta0, beta1, f_host, rhs_direction};
+  return host_pipeline(grid, plan, in, u_host, B, chunk, opts, iterations, final_rel, status, rhs_projected,
+                       history, workspace, workspace_bytes, stream);
+}
+
+int32_t chk_sample_cells(const chk_grid* grid, const uint64_t* keys, double coverage_prob, int32_t contrast_kind,
+                         double beta0, double beta1, double* beta, int32_t B, void* stream) {
+  Geo g;
+  int rc = check_grid(grid, &g);
+  if (rc) return rc;
+  if (!keys || !beta || B < 1) return fail(CHK_EINVAL, "bad arguments");
+  if (contrast_kind != CHK_CONTRAST_FIXED && contrast_kind != CHK_CONTRAST_TWO_VALUE)
+    return fail(CHK_EINVAL, "contrast_kind must be CHK_CONTRAST_FIXED or CHK_CONTRAST_TWO_VALUE");
+  const int ncell = g.L * g.L * g.L;
+  const int gx = (int)std::min<long long>(((long long)ncell / 4 + 255) / 256 + 1, 1184);
+  sample_cells_kernel<<<dim3(gx, B), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      keys, ncell, coverage_prob, contrast_kind, beta0, beta1, beta);
+  CHK_LAUNCHED();
+  return CHK_OK;
 }
 
 }  // extern "C"
@@ -1050,7 +1156,7 @@ int32_t chk_slab_phase(const chk_grid* grid, const chk_precond_plan* plan, const
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PlanDev pl = plan_dev(plan);
   SolveCtl ctl{w.st, w.Rh, w.part, w.hist, maxblk_of(n), opts->max_iter, opts->tol,
-               opts->precond_residual_stopping ? 1 : 0, 0, red, 1};
+               opts->precond_residual_stopping ? 1 : 0, red, 1};
   double2* XA = static_cast<double2*>(xa);
   double2* XB = static_cast<double2*>(xb);
   const double ntot = (double)n * n * n;

@@ -250,31 +250,6 @@ struct FftStop {
     }
   }
 };
-// fft_smem with the last two stages (a contiguous block of BL elements per pencil)
-// fused in registers when FUSE: same arithmetic in the same order, one shared-memory
-// pass and one barrier fewer.  Same contract as fft_smem (sync before; returns synced).
-template <int N, bool INV, int NP, bool FUSE, class Addr>
-__device__ __forceinline__ void fft_smem_rows(double2* buf, const Addr& addr, const double2* __restrict__ tw,
-                                              int ntab) {
-  if constexpr (!FUSE) {
-    fft_smem<N, INV, NP>(buf, addr, tw, ntab);
-  } else {
-    constexpr int BL = LastTwo<N>::value;
-    static_assert(BL > 1 && BL <= 16, "register block of the last two stages");
-    if constexpr (!INV) FftStop<N, N, false, NP, BL>::run(buf, addr, tw, ntab / N);
-    for (int item = threadIdx.x; item < NP * (N / BL); item += blockDim.x) {
-      const int p = item % NP, blk = item / NP;
-      double2 v[BL];
-#pragma unroll
-      for (int e = 0; e < BL; ++e) v[e] = buf[addr(p, blk * BL + e)];
-      RegFft<BL, BL, INV>::run(v, tw, ntab);  // twiddle (j m) ntab / M as in fft_stage
-#pragma unroll
-      for (int e = 0; e < BL; ++e) buf[addr(p, blk * BL + e)] = v[e];
-    }
-    __syncthreads();
-    if constexpr (INV) FftStop<N, N, true, NP, BL>::run(buf, addr, tw, ntab / N);
-  }
-}
 
 // ----------------------------------------------------------------------------
 // reductions (deterministic: fixed shuffle tree, fixed warp order)

@@ -35,23 +35,11 @@
 #ifndef CHK_MARCH_S0  // marching stencil: specialised body for planes whose x0 - 1 is in the same cell
 #define CHK_MARCH_S0 1
 #endif
-#ifndef CHK_MARCH_DEDUP  // cell-row de-duplication inside the plane passes' marching stencil
-#define CHK_MARCH_DEDUP 0
-#endif
-#ifndef CHK_FUSE2  // n = 256 plane passes: last two x2 FFT stages (radix 8 x 2) fused in registers;
-#define CHK_FUSE2 0  // off: spills under the 80-register / 3-CTA bound (config 4 fwd +1 %, inv +7 %)
-#endif
 #ifndef CHK_MID_RPF
 #define CHK_MID_RPF 1
 #endif
 #ifndef CHK_FUSED_PF  // n = 512 middle pass: L2 prefetch of the residual / diagonal tile at the
 #define CHK_FUSED_PF 1  // start of each realization
-#endif
-#ifndef CHK_FUSED_QPF  // n = 512 middle pass: L2 prefetch of the Q' rows of the CTA one wave ahead
-#define CHK_FUSED_QPF 0
-#endif
-#ifndef CHK_FUSED_AHEAD  // CTAs per wave of the n = 512 middle pass (one 512-thread CTA per SM)
-#define CHK_FUSED_AHEAD 148
 #endif
 #ifndef CHK_SC_FENCE
 #define CHK_SC_FENCE 0
@@ -111,29 +99,19 @@ struct SlabGeo {
 // Interleaved spectrum layout (n >= 256): a plane chunk is stored [ncols/W][G][W]
 // instead of [G][ncols], so that one x0 row of a middle-pass tile (W columns of
 // all G groups) is G*W*16 = 256 contiguous bytes, while the plane passes move
-// pieces of IlC*W*16 = 32 bytes (whole DRAM sectors; the G CTAs of a plane run
-// together).  n = 256: W = 2, each CTA moves its own pieces.  n = 512: W = 1, the
-// CTAs of groups (2h, 2h+1) form a 2-CTA cluster and each moves the 32-byte
-// pieces of both groups for half of the columns, exchanging the other group's
-// half through distributed shared memory (16-byte pieces would cost a
-// read-modify-write per sector).  Measured access patterns
+// pieces of W*16 = 32 bytes (whole DRAM sectors; the G CTAs of a plane run
+// together).  n = 256: W = 2, each CTA moves its own pieces.  Measured access patterns
 // (tools/chunk_probe.cu): tile rows of 16 B 2.3 TB/s, 32 B 3.5 TB/s, 256 B
 // 6.3 TB/s; 32 B plane pieces 6.0 (write) / 5.6 (read) TB/s vs 7.4 contiguous,
 // 16 B pieces 1.1 / 3.5 TB/s.  IlW = 0: the contiguous [G][ncols] layout.
-// n = 512 default: contiguous layout (CHK_IL512=0).  Measured on config 5 with 512
-// threads per CTA: the clustered interleaved layout speeds the middle pass up by
-// only 5 % (it runs one CTA per SM, latency-bound) while the cluster barriers and
-// synchronous piece loads slow the plane passes by 17 % / 38 % (2.11e10 vs
-// 2.28e10 DOF-it/s); the clustered path stays selectable for experiments.
-#ifndef CHK_IL512
-#define CHK_IL512 0
-#endif
+// n = 512: contiguous layout.  (A 2-CTA-cluster interleaved variant exchanging the
+// 16-byte pieces through DSMEM measured 8 % slower on config 5 and was removed.)
 #ifndef CHK_NT512
 #define CHK_NT512 512
 #endif
 template <int N>
 struct IlW {
-  static constexpr int value = (N == 256) ? 2 : ((N == 512 && CHK_IL512) ? 1 : 0);
+  static constexpr int value = (N == 256) ? 2 : 0;
 };
 // threads per CTA of the plane passes and the fused middle pass: n = 512 runs one
 // CTA per SM (131 KB slab), so it takes more warps per CTA
@@ -155,10 +133,6 @@ struct MidNT {
   static constexpr int minb = (N == 512) ? 1 : 2;
   static constexpr int minb_dg = (N == 512) ? 1 : 3;  // diagonal read from L2: tile-only smem
 };
-template <int N>
-struct IlC {  // CTAs per cluster of the plane passes
-  static constexpr int value = (N == 512 && CHK_IL512) ? 2 : 1;
-};
 
 // start of the (s, b, x0l, g) row chunk of an exchange buffer (complex units)
 __host__ __device__ __forceinline__ size_t slab_row(const SlabGeo& sg, int B, int G, int s, int b, int x0l,
@@ -175,7 +149,6 @@ struct SolveCtl {
   int max_iter;
   double tol;
   int prs;           // precond_residual_stopping
-  int dbg;           // timing experiments only (CHK_DEBUG_FLAGS), 0 in production
   double* red;       // [B][4] rank-local sums (slab mode), null otherwise
   int red_only;      // slab mode: last CTAs publish rank-local sums, decisions after allreduce
 };
@@ -233,16 +206,8 @@ __device__ __forceinline__ int dig_freq(int p) {
 #ifndef CHK_R256
 #define CHK_R256 1
 #endif
-// n = 512 (CHK_R512=1): 2, 8, 2, 8, 2 -- radix-2 first stage shared with the group
-// combine (mid_column_r512_kernel), then two register-fused radix-16 passes.  Off by
-// default: measured 2105 us vs 2001 us for mid_column_fused on config 5 (128-register
-// cap at 512 threads spills; the scattered 16-byte row loads become MIO-throttled).
-#ifndef CHK_R512
-#define CHK_R512 0
-#endif
 __host__ __device__ constexpr int x0_radix(int N, int M) {
   return (N == 256 && CHK_R256)   ? ((M == 256 || M == 2) ? 2 : 8)
-         : (N == 512 && CHK_R512) ? ((M == 512 || M == 32 || M == 2) ? 2 : 8)
                                   : ((M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2));
 }
 // frequency held at position p after the forward x0 transform (x0_radix order)
@@ -962,7 +927,7 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
       else if (s1)
         stencil_march<N, G, NR, false, false, false, true>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
       else
-        stencil_march<N, G, NR, false, CHK_MARCH_DEDUP>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
+        stencil_march<N, G, NR, false, false>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
     } else {
       for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
         const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
@@ -979,7 +944,7 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
         if (ctl.red_only) {
           ctl.red[4 * b] = t0;  // rank-local p.Ap, decided after the allreduce
         } else {
-          if ((!(t0 > 0.0) || !isfinite(t0)) && !ctl.dbg) {  // solver.py:164-165
+          if ((!(t0 > 0.0) || !isfinite(t0))) {  // solver.py:164-165
             st->status = ST_BREAKDOWN;
             st->iters = it;
           }
@@ -990,9 +955,8 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
     }
   }
   __syncthreads();
-  if (MODE == FWD_Q && (ctl.dbg & 1)) return;  // debug: skip the transform phase
   // R2C along x2: rows of N reals viewed as N/2 complex (z_m = x_2m + i x_2m+1)
-  fft_smem_rows<N2, false, NR, (N == 256 && CHK_FUSE2)>(buf, RowAddr{HP}, pl.tw, N);
+  fft_smem<N2, false, NR>(buf, RowAddr{HP}, pl.tw, N);
   r2c_post<N>(buf, NR, HP, pl.tw);
   __syncthreads();
   // C2C along the x1 group (length NR)
@@ -1003,9 +967,9 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   __syncthreads();
   if constexpr (IlW<N>::value > 0) {
     // interleaved layout: 32-byte pieces at a stride of G*W complex
-    constexpr int IW = IlW<N>::value, CL = IlC<N>::value;
-    static_assert(IW * CL == 2, "pieces are two complex values");
-    if constexpr (CL == 1) {
+    constexpr int IW = IlW<N>::value;
+    static_assert(IW == 2, "pieces are two complex values");
+    {
       const int npc = sg.ncols / IW;
       for (int c = 0; c < sg.P; ++c) {
         double* dst = reinterpret_cast<double*>(S + slab_row(sg, B, G, c, b, x0l, 0) + gg * IW);
@@ -1017,26 +981,6 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
           stv4(dst + (size_t)i * 2 * G * IW, v);
         }
       }
-    } else {
-      // 2-CTA cluster (groups g0, g0 + 1): this CTA stores columns [r*h, (r+1)*h) of both
-      cluster_sync_all();  // both slabs complete
-      const int r = (int)cluster_rank();
-      const int g0 = gg - r;
-      const uint32_t other = dsmem_map(buf, (uint32_t)(r ^ 1));
-      const int h = sg.ncols / 2;
-      for (int c = 0; c < sg.P; ++c) {
-        double* dst = reinterpret_cast<double*>(S + slab_row(sg, B, G, c, b, x0l, 0) + g0);
-#pragma unroll 4
-        for (int i = r * h + threadIdx.x; i < (r + 1) * h; i += blockDim.x) {
-          const int e = c * sg.ncols + i;
-          const double2 mine = buf[e];
-          const double2 theirs = dsmem_ld2(other + (uint32_t)e * 16u);
-          const double2 lo = r ? theirs : mine, hi = r ? mine : theirs;
-          const double v[4] = {lo.x, lo.y, hi.x, hi.y};
-          stv4(dst + (size_t)i * 2 * G, v);
-        }
-      }
-      cluster_sync_all();  // the partner has read this CTA's slab
     }
     return;
   }
@@ -1092,7 +1036,7 @@ __device__ __forceinline__ void mid_decide(RState* st, const SolveCtl& ctl, int 
   const double rel = sqrt(rr) / st->normf;  // solver.py:171
   if (ctl.hist) ctl.hist[(size_t)b * ctl.max_iter + (it - 1)] = rel;
   st->final_rel = rel;
-  if (!isfinite(rel) && !ctl.dbg) {  // solver.py:172-173
+  if (!isfinite(rel)) {  // solver.py:172-173
     st->status = ST_BREAKDOWN;
     st->iters = it;
     return;
@@ -1219,7 +1163,7 @@ __global__ void __launch_bounds__(256) dtile_kernel(PlanDev pl, double* __restri
 // tile (16-byte async copies of the precomputed tile, or evaluated in place).
 template <int N, int G, int W, int MODE>
 __device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, const PlanDev& pl,
-                                             int* s_k1, int* s_k2, double* s_wgt, double2* s_tw, int dbg = 0) {
+                                             int* s_k1, int* s_k2, double* s_wgt, double2* s_tw) {
   constexpr int GW = G * W;
   mid_slots<N, G, W>(c0, pl, s_k1, s_k2, s_wgt, s_tw);
   if (pl.D) {
@@ -1229,7 +1173,6 @@ __device__ __forceinline__ void mid_prologue(double2* buf, double* Dsm, int c0, 
     cp_async_wait_all();
   }
   __syncthreads();
-  if (dbg & 16) return;  // timing experiment: no diagonal tile
   if (!pl.D) {
     mid_dtile<N, G, W>(reinterpret_cast<double*>(buf), Dsm, pl, s_k1, s_k2);
   }
@@ -1321,14 +1264,13 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
     __syncthreads();
     Dg = pl.D + (size_t)(cg0 / W) * N * GW;
   } else {
-    mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
+    mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw);
   }
   const double scale = 2.0 / ((double)N * N * N);
   if (CHK_FUSED_PF && DG && threadIdx.x >= 32 && threadIdx.x < 36) {  // diagonal tile -> L2 (first use: fused last stage)
     constexpr uint32_t q = N * GW * sizeof(double) / 4;
     bulk_prefetch_l2(reinterpret_cast<const char*>(Dg) + (threadIdx.x - 32) * q, q);
   }
-  bool ahead_done = false;
   for (int j = 0; j < NB; ++j) {
     if (!s_act[j]) continue;
     const int b = b0 + j;
@@ -1348,26 +1290,6 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
       reg_fft<G, false>(v, pl.tw, N);
 #pragma unroll
       for (int g = 0; g < G; ++g) buf[x0 * RS + g * W + w] = v[g];
-    }
-    if (CHK_FUSED_QPF && !ahead_done) {
-      // Q' rows of the CTA one wave ahead -> L2 while this CTA runs its shared-memory
-      // stages (one CTA per SM: nothing else would overlap the next CTA's loads)
-      ahead_done = true;
-      const int na = blockIdx.x + CHK_FUSED_AHEAD;
-      if (na < (int)gridDim.x) {
-        const int bga = na / TILES, tla = na - bga * TILES;
-        const int c0a = tla * W;
-        for (int ja = 0; ja < NB; ++ja) {
-          const int ba = bga * NB + ja;
-          if (ba >= B || (MODE != MID_APPLY && ctl.st[ba].status != ST_ACTIVE)) continue;
-          for (int item = threadIdx.x; item < N * W; item += blockDim.x) {
-            const int w = item % W, x0 = item / W;
-            const size_t rbase = slab_row(sg, B, G, x0 >> nsh, ba, x0 & (sg.nloc - 1), 0) + (IL ? c0a * G : c0a) + w;
-#pragma unroll
-            for (int g = 0; g < G; ++g) asm volatile("prefetch.global.L2 [%0];" ::"l"(S + rbase + (size_t)g * GSTR));
-          }
-        }
-      }
     }
     __syncthreads();
     FftRecButLast<N, N, false, GW>::run(buf, X0Addr{RS}, pl.tw, 1);
@@ -1606,210 +1528,6 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
   }
 }
 
-#if CHK_R512
-// ----------------------------------------------------------------------------
-// kernel 2d: register-phase spectral column pass for n = 512 (x0 radix 2, 8, 2, 8, 2)
-// ----------------------------------------------------------------------------
-// CTA (512 threads, one per SM: the 139 KB tile) = NB realizations x one tile (W = 1
-// column x G = 16 groups = 16 slots, 512 x0 positions; contiguous spectrum layout).
-//   A  (thread = x0 row; rows j and j + 256 in lanes l, l ^ 16 of one warp): group
-//      combine in registers + the radix-2 x0 stage (M = 512) by shuffle   -> smem
-//   B1 (thread = slot, 256-block, offset j0 < 16): radix-8 stage M = 256 and radix-2
-//      stage M = 32 in registers (16 positions j0 + 16 m)               smem -> smem
-//   B2 (thread = slot, 16-block): radix-8 (M = 16) + radix-2 (M = 2), residual
-//      update / diagonal (plan table) / Parseval, inverse                 smem -> smem
-//   B1' inverse M = 32 + M = 256 stages;  A' inverse radix-2 + group combine -> HBM
-// Fusing consecutive DIF stages in registers does the same arithmetic in the same
-// order as separate stages.  8 shared-memory passes per element (mid_column_fused: 12).
-#ifndef CHK_R512_RPF
-#define CHK_R512_RPF 1
-#endif
-template <int NB, int MODE>
-__global__ void __launch_bounds__(512, 1) mid_column_r512_kernel(double2* __restrict__ S, PlanDev pl, SolveCtl ctl,
-                                                                 SlabGeo sg, int it, int B) {
-  constexpr int N = 512, G = 16, W = 1, GW = G * W, RS = GW + 1;
-  static_assert(IlW<N>::value == 0, "contiguous spectrum layout expected at n = 512");
-  static_assert(x0_radix(N, 512) == 2 && x0_radix(N, 256) == 8 && x0_radix(N, 32) == 2 && x0_radix(N, 16) == 8 &&
-                    x0_radix(N, 2) == 2,
-                "x0 radix order 2, 8, 2, 8, 2");
-  const int TILES = sg.tiles;
-  const int nsh = __ffs(sg.nloc) - 1;
-  const size_t GSTR = (size_t)sg.ncols;
-  extern __shared__ double2 buf[];  // [N][RS]
-  __shared__ double scratch[64];
-  __shared__ int s_k1[GW], s_k2[GW];
-  __shared__ double s_wgt[GW];
-  __shared__ double2 s_tw[GW];
-  __shared__ int s_act[NB];
-  __shared__ double s_alpha[NB];
-  __shared__ double s_wsum[NB * 16 * 2];
-  __shared__ int s_dc;
-  const int bg = blockIdx.x / TILES;
-  const int tile = blockIdx.x - bg * TILES;
-  const int c0 = tile * W;
-  const int cg0 = (sg.tile_off + tile) * W;
-  const int b0 = bg * NB;
-  if (threadIdx.x == 0) {
-    int any = 0;
-    for (int j = 0; j < NB; ++j) {
-      const int b = b0 + j;
-      int a = (b < B);
-      if (a && MODE != MID_APPLY) a = (ctl.st[b].status == ST_ACTIVE);
-      s_act[j] = a;
-      s_alpha[j] = (a && MODE == MID_ITER) ? ctl.st[b].alpha : 0.0;
-      any |= a;
-    }
-    scratch[0] = any;
-    s_dc = -1;
-  }
-  __syncthreads();
-  if (scratch[0] == 0.0) return;
-  mid_slots<N, G, W>(cg0, pl, s_k1, s_k2, s_wgt, s_tw);
-  __syncthreads();
-  if (MODE != MID_APPLY && threadIdx.x < GW && s_k1[threadIdx.x] == 0 && s_k2[threadIdx.x] == 0)
-    s_dc = threadIdx.x;
-  __syncthreads();
-  const double* Dg = pl.D + (size_t)(cg0 / W) * N * GW;
-  if (CHK_R512_RPF && threadIdx.x >= 32 && threadIdx.x < 36) {  // diagonal tile -> L2 (read in B2)
-    constexpr uint32_t q = N * GW * sizeof(double) / 4;
-    bulk_prefetch_l2(reinterpret_cast<const char*>(Dg) + (threadIdx.x - 32) * q, q);
-  }
-  const double scale = 2.0 / ((double)N * N * N);
-  // phase A item: x0 pair jA, jA + 256 in lanes l and l ^ 16 of one warp (row x0A = jA + 256 hA)
-  const int hA = (threadIdx.x >> 4) & 1, jA = (threadIdx.x >> 5) * 16 + (threadIdx.x & 15);
-  const int x0A = jA + 256 * hA;
-  for (int j = 0; j < NB; ++j) {
-    if (!s_act[j]) continue;
-    const int b = b0 + j;
-    if (CHK_R512_RPF && MODE == MID_ITER && threadIdx.x < 4) {  // residual tile -> L2 before B2 reads it
-      constexpr uint32_t q = N * GW * sizeof(double2) / 4;
-      bulk_prefetch_l2(reinterpret_cast<const char*>(ctl.Rh + ((size_t)b * TILES + tile) * N * GW) + threadIdx.x * q, q);
-    }
-    // ---- A: loads, group combine, radix-2 stage (M = 512; partner row by shuffle) ----
-    {
-      double2 v[G];
-      const size_t rbase = slab_row(sg, B, G, x0A >> nsh, b, x0A & (sg.nloc - 1), 0) + c0;
-#pragma unroll
-      for (int g = 0; g < G; ++g) v[g] = S[rbase + (size_t)g * GSTR];
-#pragma unroll
-      for (int g = 1; g < G; ++g) v[g] = cmul(v[g], s_tw[g]);
-      reg_fft<G, false>(v, pl.tw, N);
-      const double2 t1 = __ldg(pl.tw + jA);
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const double2 o = make_double2(__shfl_xor_sync(0xffffffffu, v[g].x, 16), __shfl_xor_sync(0xffffffffu, v[g].y, 16));
-        buf[x0A * RS + g] = hA ? cmul(csub(o, v[g]), t1) : cadd(v[g], o);
-      }
-    }
-    __syncthreads();
-    // ---- B1: radix-8 stage M = 256 (stride 32) + radix-2 stage M = 32 (stride 16) ----
-    const int sB = threadIdx.x % GW, j0 = (threadIdx.x / GW) % 16, blkB = threadIdx.x / (16 * GW);
-    double2* baseB = buf + (blkB * 256 + j0) * RS + sB;  // position blk*256 + j0 + 16 (c + 2 t) -> v[c][t]
-    {
-      double2 v[2][8];
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int t = 0; t < 8; ++t) v[c][t] = baseB[(16 * c + 32 * t) * RS];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        dftR<8, false>(v[c]);
-        const int jj = j0 + 16 * c;
-        if (jj > 0) {
-#pragma unroll
-          for (int m = 1; m < 8; ++m) v[c][m] = cmul(v[c][m], __ldg(pl.tw + jj * m * 2));
-        }
-      }
-      const double2 t2 = __ldg(pl.tw + j0 * 16);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const double2 a = cadd(v[0][t], v[1][t]);
-        const double2 d = csub(v[0][t], v[1][t]);
-        baseB[(32 * t) * RS] = a;
-        baseB[(16 + 32 * t) * RS] = j0 > 0 ? cmul(d, t2) : d;
-      }
-    }
-    __syncthreads();
-    // ---- B2: last two stages, residual / diagonal / Parseval, first two inverse stages ----
-    double rr = 0.0, rz = 0.0;
-    {
-      const int s = threadIdx.x % GW, blk = threadIdx.x / GW;  // 32 blocks of 16 positions
-      double2* row = buf + (blk * 16) * RS + s;
-      double2 v[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = row[e * RS];
-      reg_fft<16, false>(v, pl.tw, N);
-      double2* Rt = ctl.Rh + ((size_t)b * TILES + tile) * N * GW + (blk * 16) * GW + s;
-      const double wgt = s_wgt[s];
-      const double al = s_alpha[j];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int pos0 = blk * 16 + e;
-        // mean projection of z (solver.py:153,179): the zero-frequency coefficient is 0
-        const double D = (pos0 == 0 && s == s_dc) ? 0.0 : __ldg(Dg + pos0 * GW + s);
-        v[e] = mid_point<MODE>(v[e], D, wgt, scale, al, Rt + e * GW, rr, rz);
-      }
-      reg_fft<16, true>(v, pl.tw, N);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) row[e * RS] = v[e];
-    }
-    __syncthreads();
-    // ---- B1': inverse M = 32 stage, inverse M = 256 stage ----
-    {
-      double2 v[2][8];
-      const double2 t2 = __ldg(pl.tw + j0 * 16);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const double2 a = baseB[(32 * t) * RS];
-        const double2 d0 = baseB[(16 + 32 * t) * RS];
-        const double2 d = j0 > 0 ? cmulc(d0, t2) : d0;
-        v[0][t] = cadd(a, d);
-        v[1][t] = csub(a, d);
-      }
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int jj = j0 + 16 * c;
-        if (jj > 0) {
-#pragma unroll
-          for (int m = 1; m < 8; ++m) v[c][m] = cmulc(v[c][m], __ldg(pl.tw + jj * m * 2));
-        }
-        dftR<8, true>(v[c]);
-      }
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int t = 0; t < 8; ++t) baseB[(16 * c + 32 * t) * RS] = v[c][t];
-    }
-    __syncthreads();
-    // ---- A': inverse radix-2 stage (partner row by shuffle), inverse group combine, store ----
-    {
-      double2 v[G];
-      const double2 t1 = __ldg(pl.tw + jA);
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const double2 x = hA ? cmulc(buf[x0A * RS + g], t1) : buf[x0A * RS + g];
-        const double2 o = make_double2(__shfl_xor_sync(0xffffffffu, x.x, 16), __shfl_xor_sync(0xffffffffu, x.y, 16));
-        v[g] = hA ? csub(o, x) : cadd(x, o);
-      }
-      reg_fft<G, true>(v, pl.tw, N);
-#pragma unroll
-      for (int g = 1; g < G; ++g) v[g] = cmulc(v[g], s_tw[g]);
-      const size_t rbase = slab_row(sg, B, G, x0A >> nsh, b, x0A & (sg.nloc - 1), 0) + c0;
-#pragma unroll
-      for (int g = 0; g < G; ++g) S[rbase + (size_t)g * GSTR] = v[g];
-    }
-    if (MODE != MID_APPLY) warp_partials(rr, rz, s_wsum, j);
-    __syncthreads();
-  }
-  if (MODE != MID_APPLY) {
-    const double inv = 1.0 / ((double)N * N * N);  // Parseval: (1/N^3) sum conj(X) Y
-    mid_tickets<NB>(s_wsum, s_act, b0, tile, TILES, ctl, scratch, [&](int b, double t0, double t1) {
-      mid_decide(ctl.st + b, ctl, b, it, t0 * inv, t1 * inv);
-    });
-  }
-}
-
-#endif  // CHK_R512
 
 // ----------------------------------------------------------------------------
 // kernel 2b: register-resident spectral column pass (n <= 128)
@@ -1938,7 +1656,7 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
 #pragma unroll
     for (int e = 0; e < RB; ++e) Dreg[e] = (blk * RB + e == 0 && s == s_dc) ? 0.0 : __ldg(Dg + e * GW);
   } else {
-    mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw, ctl.dbg);
+    mid_prologue<N, G, W, MODE>(buf, Dsm, cg0, pl, s_k1, s_k2, s_wgt, s_tw);
   }
 
   const double scale = 2.0 / ((double)N * N * N);
@@ -1999,17 +1717,6 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
         }
       }
       double2* dst = buf + pr * N * RS;
-      if (ctl.dbg & 32) {  // timing experiment: registers straight back out
-        const int bb2 = b0 + c * P + pr;
-#pragma unroll
-        for (int t = 0; t < RA; ++t)
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const int x0 = j + JA * t;
-            S[slab_row(sg, B, G, x0 >> nsh, bb2, x0 & (sg.nloc - 1), g) + c0 + w] = v[g][t];
-          }
-        continue;
-      }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         dftR<RA, false>(v[g]);
@@ -2036,7 +1743,6 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
       double2 v[RB];
 #pragma unroll
       for (int e = 0; e < RB; ++e) v[e] = row[e * RS];
-      if (ctl.dbg & 8) continue;  // timing experiment: no phase-B work
       reg_fft<RB, false>(v, pl.tw, ntab);
       double rr = 0.0, rz = 0.0;
       const double wgt = s_wgt[s];
@@ -2184,8 +1890,8 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     }
     if (!do_p && !do_u) return;
   }
-  constexpr int IW = IlW<N>::value, CL = IlC<N>::value;
-  if constexpr (IW > 0 && CL == 1) {
+  constexpr int IW = IlW<N>::value;
+  if constexpr (IW > 0) {
     if (do_p) {
       // interleaved layout: 16-byte cp.async copies of the 32-byte pieces
       for (int c = 0; c < sg.P; ++c) {
@@ -2195,29 +1901,6 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
           cp_async16(dst + i, src + (size_t)(i / IW) * G * IW + (i % IW));
       }
       cp_async_commit();
-    }
-  } else if constexpr (IW > 0) {
-    static_assert(IW == 1 && CL == 2, "cluster pieces: two groups of one column");
-    if (do_p) {  // uniform over the cluster (one realization)
-      // 2-CTA cluster: this CTA loads the 32-byte pieces (both groups) of columns
-      // [r*h, (r+1)*h) and delivers the partner's group through DSMEM
-      cluster_sync_all();  // the partner is running (its window may be written)
-      const int r = (int)cluster_rank();
-      const int g0 = gg - r;
-      const uint32_t other = dsmem_map(buf, (uint32_t)(r ^ 1));
-      const int h = sg.ncols / 2;
-      for (int c = 0; c < sg.P; ++c) {
-        const double* src = reinterpret_cast<const double*>(S + slab_row(sg, B, G, c, b, x0, 0) + g0);
-#pragma unroll 4
-        for (int i = r * h + threadIdx.x; i < (r + 1) * h; i += blockDim.x) {
-          double v[4];
-          ldv4(src + (size_t)i * 2 * G, v);
-          const int e = c * sg.ncols + i;
-          const double2 lo = make_double2(v[0], v[1]), hi = make_double2(v[2], v[3]);
-          buf[e] = r ? hi : lo;
-          dsmem_st2(other + (uint32_t)e * 16u, r ? lo : hi);
-        }
-      }
     }
   } else if (do_p) {
     // the slab row arrives as P column chunks (one bulk load each)
@@ -2236,11 +1919,9 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     bulk_prefetch_l2(u + ro, N * sizeof(double));
   }
   if (do_p) {
-    if constexpr (IW > 0 && CL == 1) {
+    if constexpr (IW > 0) {
       cp_async_wait_all();
       __syncthreads();
-    } else if constexpr (IW > 0) {
-      cluster_sync_all();  // both halves delivered
     } else {
       __syncthreads();  // barrier initialised before anyone waits
       mbar_wait(&bar, 0);
@@ -2248,7 +1929,7 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     fft_smem<NR, true, H>(buf, ColAddr{HP}, pl.tw, N);
     c2r_pre<N>(buf, NR, HP, pl.tw);
     __syncthreads();
-    fft_smem_rows<N2, true, NR, (N == 256 && CHK_FUSE2)>(buf, RowAddr{HP}, pl.tw, N);
+    fft_smem<N2, true, NR>(buf, RowAddr{HP}, pl.tw, N);
   }
   const double* sm = reinterpret_cast<const double*>(buf);
   constexpr int Q4 = N / 4;
@@ -2385,7 +2066,7 @@ __global__ void decide_kernel(SolveCtl ctl, const double* __restrict__ red, int 
     } else if (st->status == ST_ACTIVE) {
       if (what == DECIDE_ALPHA) {
         const double pq = red[4 * b];
-        if ((!(pq > 0.0) || !isfinite(pq)) && !ctl.dbg) {  // solver.py:164-165
+        if ((!(pq > 0.0) || !isfinite(pq))) {  // solver.py:164-165
           st->status = ST_BREAKDOWN;
           st->iters = it;
         }

@@ -151,11 +151,14 @@ class DevicePlan:
     """Owns a chk_precond_plan (device twiddles + factors / eigenvalues)."""
 
     def __init__(self, kind: str, n: int, tensor: CanonicalTensor | None = None,
-                 delta: float = 0.0):
+                 delta: float = 0.0, eps_rank: float = 0.0):
+        torch = _lib.require_cuda()
         lib = _lib.load()
         self.kind = kind
         self.n = n
         self.delta = float(delta)
+        self.eps_rank = float(eps_rank)
+        self.device = int(torch.cuda.current_device())  # the plan's buffers live here
         handle = ctypes.c_void_p()
         eig = np.ascontiguousarray(fourier_eigenvalues(n).values, dtype=np.float64)
         if kind == "lkr":
@@ -184,14 +187,24 @@ class DevicePlan:
         return int(_lib.load().chk_precond_workspace_bytes(self.handle, B))
 
 
+def _plan_for(d: int, n: int, kind: str, eps_rank: float, delta: float, device: int | None = None) -> DevicePlan:
+    """Cached device plan, keyed by the CUDA device it lives on (current device
+    when ``device`` is None)."""
+    if device is None:
+        device = int(_lib.require_cuda().cuda.current_device())
+    return _plan_on(d, n, kind, eps_rank, delta, int(device))
+
+
 @functools.lru_cache(maxsize=8)
-def _plan_for(d: int, n: int, kind: str, eps_rank: float, delta: float) -> DevicePlan:
+def _plan_on(d: int, n: int, kind: str, eps_rank: float, delta: float, device: int) -> DevicePlan:
     if d != 3:
         raise ValueError("the GPU path implements d = 3 only")
-    if kind == "lkr":
-        t = dc_correction(canonical_reciprocal(fourier_eigenvalues(n), d, eps_rank))
-        return DevicePlan("lkr", n, t)
-    return DevicePlan(kind, n, delta=delta)
+    torch = _lib.require_cuda()
+    with torch.cuda.device(device):
+        if kind == "lkr":
+            t = dc_correction(canonical_reciprocal(fourier_eigenvalues(n), d, eps_rank))
+            return DevicePlan("lkr", n, t, eps_rank=eps_rank)
+        return DevicePlan(kind, n, delta=delta)
 
 
 def _device_apply(plan: DevicePlan, x):
@@ -211,14 +224,16 @@ def _device_apply(plan: DevicePlan, x):
         B = shape[0]
     else:
         raise ValueError(f"expected vector of length {size}, got shape {shape}")
-    xd = xt.to("cuda").contiguous()
-    zd = torch.empty_like(xd)
-    ws = torch.empty(plan.workspace_bytes(B), dtype=torch.uint8, device=xd.device)
-    lib = _lib.load()
-    _lib.check(lib.chk_precond_apply(plan.handle, ctypes.c_void_p(xd.data_ptr()),
-                                     ctypes.c_void_p(zd.data_ptr()), B,
-                                     ctypes.c_void_p(ws.data_ptr()), ws.numel(),
-                                     _lib.stream_handle()))
+    dev = torch.device("cuda", plan.device)
+    with torch.cuda.device(dev):
+        xd = xt.to(dev).contiguous()
+        zd = torch.empty_like(xd)
+        ws = torch.empty(plan.workspace_bytes(B), dtype=torch.uint8, device=dev)
+        lib = _lib.load()
+        _lib.check(lib.chk_precond_apply(plan.handle, ctypes.c_void_p(xd.data_ptr()),
+                                         ctypes.c_void_p(zd.data_ptr()), B,
+                                         ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                         _lib.stream_handle()))
     if is_np:
         return zd.cpu().numpy()
     return zd
@@ -238,7 +253,8 @@ _TENSOR_PLANS: dict = {}
 
 
 def _tensor_plan(t: CanonicalTensor) -> DevicePlan:
-    key = id(t)
+    torch = _lib.require_cuda()
+    key = (id(t), int(torch.cuda.current_device()))
     hit = _TENSOR_PLANS.get(key)
     if hit is not None and hit[0] is t:
         return hit[1]

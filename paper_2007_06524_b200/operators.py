@@ -76,6 +76,7 @@ class StiffnessOperator:
     .shape, .lam, .matrix(), .apply())."""
 
     def __init__(self, r: Realization):
+        r = Realization.coerce(r)
         self.realization = r
         self.config = r.config
         self.lam = float(r.config.lam)
@@ -114,5 +115,6 @@ class StiffnessOperator:
 
 def assemble_stiffness(r: Realization, agglomerate: bool = True) -> StiffnessOperator:
     """Drop-in for operators.py:278-285 (``agglomerate`` is accepted and ignored:
-    the matrix-free operator has no Kronecker terms to merge)."""
+    the matrix-free operator has no Kronecker terms to merge).  ``r`` may be a
+    realization built by the reference package itself (same fields)."""
     return StiffnessOperator(r)

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import functools
+import re
 import warnings
 from dataclasses import dataclass
 
@@ -68,10 +69,17 @@ class Preconditioner:
     plan: object = None
 
 
+def _device_index() -> int:
+    torch = _lib.require_cuda()
+    return int(torch.cuda.current_device())
+
+
 @functools.lru_cache(maxsize=8)
-def _cached_preconditioner(d: int, n: int, kind: str, eps_rank: float, delta: float) -> Preconditioner:
-    """solver.py:79-93 (same names; the apply is the device pipeline)."""
-    plan = _plan_for(d, n, kind, eps_rank, delta)
+def _cached_preconditioner(d: int, n: int, kind: str, eps_rank: float, delta: float,
+                           device: int = 0) -> Preconditioner:
+    """solver.py:79-93 (same names; the apply is the device pipeline).  Keyed
+    also by the CUDA device: a plan's buffers live on the device it was built on."""
+    plan = _plan_for(d, n, kind, eps_rank, delta, device)
     if kind == "fourier":
         name = "fourier"
     elif kind == "regularized":
@@ -85,7 +93,43 @@ def make_preconditioner(d: int, n: int, opts: SolveOptions) -> Preconditioner:
     """solver.py:96-100."""
     eps_rank = opts.eps_rank if opts.preconditioner == "lkr" else 0.0
     delta = opts.delta if opts.preconditioner == "regularized" else 0.0
-    return _cached_preconditioner(d, n, opts.preconditioner, eps_rank, delta)
+    return _cached_preconditioner(d, n, opts.preconditioner, eps_rank, delta, _device_index())
+
+
+_NAME_RE = {
+    "lkr": re.compile(r"^lkr\(eps=([^,]+),rank=(\d+)\)$"),
+    "regularized": re.compile(r"^regularized\(delta=([^)]+)\)$"),
+}
+
+
+def _device_preconditioner(precond, d: int, n: int) -> Preconditioner:
+    """The device-plan preconditioner equivalent to ``precond``: ours as is; a
+    reference-built ``Preconditioner(name, apply)`` from its make_preconditioner
+    (solver.py:79-100) is recognised by its name (``fourier``,
+    ``regularized(delta=...)``, ``lkr(eps=...,rank=R)``).  Any other callable has
+    no device plan: ValueError (the GPU path has no host fallback)."""
+    plan = getattr(precond, "plan", None)
+    if isinstance(plan, DevicePlan):
+        if plan.n != n:
+            raise ValueError(f"preconditioner is for n = {plan.n}, operator has n = {n}")
+        if plan.device != _device_index():
+            return make_preconditioner(d, n, SolveOptions(
+                preconditioner=plan.kind, eps_rank=plan.eps_rank or 1e-8, delta=plan.delta))
+        return precond
+    name = str(getattr(precond, "name", ""))
+    if name == "fourier":
+        return make_preconditioner(d, n, SolveOptions(preconditioner="fourier"))
+    m = _NAME_RE["regularized"].match(name)
+    if m:
+        return make_preconditioner(d, n, SolveOptions(preconditioner="regularized", delta=float(m.group(1))))
+    m = _NAME_RE["lkr"].match(name)
+    if m:
+        p = make_preconditioner(d, n, SolveOptions(preconditioner="lkr", eps_rank=float(m.group(1))))
+        if p.plan.r1 != int(m.group(2)):
+            raise ValueError(f"{name}: the rebuilt factors have rank {p.plan.r1}")
+        return p
+    raise ValueError(f"preconditioner {name!r} has no device plan: build it with make_preconditioner "
+                     f"(kinds {PRECONDITIONERS})")
 
 
 def project_mean_zero(x):
@@ -134,7 +178,8 @@ class Workspace:
     def get(self, nbytes: int, device):
         import torch
 
-        if self.buf is None or self.buf.numel() < nbytes:
+        device = torch.device(device)
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
             self.buf = None
             self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
         return self.buf
@@ -155,14 +200,11 @@ def pcg_solve_batched(A, F, opts: SolveOptions | None = None, precond: Precondit
     from .operators import StiffnessBatch, StiffnessOperator
 
     opts = opts or SolveOptions()
-    batch = A._batch if isinstance(A, StiffnessOperator) else A
-    if not isinstance(batch, StiffnessBatch):
-        raise TypeError("A must be a StiffnessBatch or StiffnessOperator")
+    batch = _as_batch(A)
     if precond is None:
         precond = make_preconditioner(3, batch.n, opts)
+    precond = _device_preconditioner(precond, 3, batch.n)
     plan = precond.plan
-    if not isinstance(plan, DevicePlan):
-        raise TypeError("precond must come from make_preconditioner (device plan)")
     n = batch.n
     size = n ** 3
     B = batch.B
@@ -205,6 +247,7 @@ def pcg_solve_host(config, beta_host, F_host, opts: SolveOptions | None = None,
     n = config.n
     if precond is None:
         precond = make_preconditioner(3, n, opts)
+    precond = _device_preconditioner(precond, 3, n)
     plan = precond.plan
     beta = beta_host if isinstance(beta_host, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(np.asarray(beta_host, dtype=np.float64)))
@@ -240,10 +283,87 @@ def pcg_solve_host(config, beta_host, F_host, opts: SolveOptions | None = None,
                        history=hist, launches=int(lib.chk_last_launch_count()))
 
 
+def pcg_solve_seeds(config, seeds, opts: SolveOptions | None = None, precond: Preconditioner | None = None,
+                    rhs=1, chunk: int | None = None, out=None, record_history: bool = True,
+                    workspace: Workspace | None = None):
+    """Seeds to solutions: realization ``seeds[m]`` is drawn on the GPU
+    (bit-identical to sample_realization), its load is the device corrector RHS
+    along direction ``rhs`` (int, the PCG load of homogenize.py:110) or row m of
+    a host array ``rhs`` (B, n^3), and u comes back to the host ``out`` (pinned
+    (B, n^3) tensor or new).  Chunked over lanes like pcg_solve_host; the
+    host-side work per realization is the SeedSequence hash of its seed."""
+    from .lattice import contrast_args, philox_keys
+
+    torch = _lib.require_cuda()
+    opts = opts or SolveOptions()
+    n = config.n
+    if precond is None:
+        precond = make_preconditioner(3, n, opts)
+    precond = _device_preconditioner(precond, 3, n)
+    plan = precond.plan
+    kind, b0, b1 = contrast_args(config)
+    keys = philox_keys(seeds)
+    B = keys.shape[0]
+    f_host = None
+    direction = 0
+    if isinstance(rhs, (int, np.integer)):
+        direction = int(rhs)
+        if not 1 <= direction <= 3:
+            raise ValueError(f"direction must be in 1..3, got {direction}")
+    else:
+        f_host = rhs if isinstance(rhs, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(np.asarray(rhs, dtype=np.float64)))
+        f_host = f_host.reshape(B, -1).contiguous()
+    U = out if out is not None else torch.empty((B, n ** 3), dtype=torch.float64).pin_memory()
+    if chunk is None:
+        chunk = max(1, (B + 7) // 8, -(-(4 << 20) // n ** 3))
+    grid = _lib.grid_struct(3, n, config.L, config.n0, config.k, config.offset, config.lam)
+    lib = _lib.load()
+    wb = int(lib.chk_pcg_host_workspace_bytes(ctypes.byref(grid), plan.handle, min(chunk, B), opts.max_iter))
+    if wb == 0:
+        raise ValueError("unsupported grid for the GPU path")
+    ws = (workspace or _default_ws).get(wb, torch.device("cuda", torch.cuda.current_device()))
+    its = np.zeros(B, np.int32)
+    fin = np.zeros(B)
+    st = np.zeros(B, np.int32)
+    proj = np.zeros(B, np.int32)
+    hist = np.zeros((B, opts.max_iter)) if record_history else None
+    copts = _lib.ChkPcgOpts(float(opts.tol), int(opts.max_iter), int(bool(opts.precond_residual_stopping)))
+    vp = ctypes.c_void_p
+    _lib.check(lib.chk_pcg_solve_seeds(
+        ctypes.byref(grid), plan.handle, keys.ctypes.data_as(vp), float(config.coverage_prob), kind, b0, b1,
+        vp(f_host.data_ptr()) if f_host is not None else None, direction, vp(U.data_ptr()), B, int(chunk),
+        ctypes.byref(copts), its.ctypes.data_as(vp), fin.ctypes.data_as(vp), st.ctypes.data_as(vp),
+        proj.ctypes.data_as(vp), hist.ctypes.data_as(vp) if hist is not None else None,
+        vp(ws.data_ptr()), ws.numel(), _lib.stream_handle()))
+    return BatchResult(u=U, iterations=its, final_residual=fin, status=st, rhs_projected=proj,
+                       history=hist, launches=int(lib.chk_last_launch_count()))
+
+
+def _as_batch(A):
+    """StiffnessBatch of ``A``: ours (StiffnessBatch / StiffnessOperator), or a
+    realization-carrying operator.  The reference's StiffnessOperator holds only
+    Kronecker terms (operators.py:96-131) -- build the device operator from the
+    same realization with ``assemble_stiffness(r)`` (ValueError otherwise)."""
+    from .operators import StiffnessBatch, StiffnessOperator
+
+    if isinstance(A, StiffnessOperator):
+        return A._batch
+    if isinstance(A, StiffnessBatch):
+        return A
+    r = getattr(A, "realization", None)
+    if r is not None:
+        return StiffnessOperator(r)._batch
+    raise ValueError(f"{type(A).__name__} is not a device stiffness operator: build it with "
+                     f"paper_2007_06524_b200.assemble_stiffness(realization)")
+
+
 def pcg_solve(A, f, opts: SolveOptions | None = None, precond: Preconditioner | None = None):
     """Drop-in for solver.py:118-194 on the GPU."""
     torch = _lib.require_cuda()
     opts = opts or SolveOptions()
+    if getattr(A, "d", 3) != 3:
+        raise ValueError("the GPU path implements d = 3 only")
     if precond is None:
         precond = make_preconditioner(A.d, A.n, opts)
     is_np = not isinstance(f, torch.Tensor)

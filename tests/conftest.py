@@ -30,7 +30,9 @@ def golden_configs(cfg_id):
     import json
 
     recs = []
-    for path in sorted(glob.glob(os.path.join(GOLDEN_DIR, f"config{cfg_id}_*.json"))):
+    full = os.path.join(GOLDEN_DIR, f"config{cfg_id}_full.json")
+    paths = [full] if os.path.exists(full) else sorted(glob.glob(os.path.join(GOLDEN_DIR, f"config{cfg_id}_*.json")))
+    for path in paths:
         recs.extend(json.load(open(path))["records"])
     recs.sort(key=lambda r: r["m"])
     return recs

@@ -7,6 +7,7 @@ records its outputs for the hot path.  The fixtures pin both the CPU oracle
     python tests/golden/make_golden.py small            # -> tests/golden/small.npz
     python tests/golden/make_golden.py config 3 0 16    # -> tests/golden/config3_0_16.json
     python tests/golden/make_golden.py formats          # -> tests/golden/formats.json
+    python tests/golden/make_golden.py pool 3 0 256 8   # -> tests/golden/config3_full.json
 
 Large arrays are never committed: for configs 2-5 we keep iteration counts,
 the full residual history, ||u||, <u, f>, <u, w> for a seeded Gaussian w and
@@ -38,6 +39,21 @@ from oracle import checkerhom_oracle as orc  # noqa: E402
 PROBE_SEED = 12345
 PROJ_SEED = 777
 N_PROBE = 4096
+
+
+N_PROJ = 16          # independent Gaussian projections per record (pool mode)
+N_PROBE_POOL = 512
+
+
+def proj_vector(N: int, k: int) -> np.ndarray:
+    """k-th projection vector w_k ~ N(0, I_N); E[(e.w_k)^2] = ||e||^2, so
+    mean_k (u.w_k - u_ref.w_k)^2 estimates ||u - u_ref||^2 (16 draws: ~+-18 %
+    on ||u - u_ref||)."""
+    return np.random.default_rng([PROJ_SEED, k]).standard_normal(N)
+
+
+def u_projections(u: np.ndarray) -> list:
+    return [float(u @ proj_vector(u.size, k)) for k in range(N_PROJ)]
 
 
 def u_probe(u: np.ndarray, f: np.ndarray) -> dict:
@@ -193,7 +209,7 @@ def small():
     print("wrote small.npz", os.path.getsize(os.path.join(HERE, "small.npz")))
 
 
-def config_run(cfg_id: int, m: int):
+def config_run(cfg_id: int, m: int, compact: bool = False):
     c = orc.CONFIGS[cfg_id]
     seed = ch.derive_seed(0, m)
     cfg = ch.LatticeConfig(d=3, L=c["L"], n0=c["n0"], alpha="1/2", lam=c["lam"])
@@ -237,6 +253,11 @@ def config_run(cfg_id: int, m: int):
            "norm_f": float(np.linalg.norm(f)), "num_covered": r.num_covered,
            "t_assembly_s": t_asm, "t_solve_s": t_solve}
     rec.update(u_probe(u, f))
+    if compact:
+        rec["u_probe"] = rec["u_probe"][:N_PROBE_POOL]
+        rec["u_proj"] = u_projections(u)
+        rec["n_proj"] = N_PROJ
+        return rec, None, None
     return rec, u, f
 
 
@@ -250,6 +271,33 @@ def configs(cfg_id: int, start: int, count: int):
         with open(path, "w") as fh:
             json.dump({"generator": "tests/golden/make_golden.py (reference checkerhom)",
                        "numpy": np.__version__, "records": recs}, fh, indent=1)
+
+
+def _pool_one(args):
+    cfg_id, m = args
+    rec, _, _ = config_run(cfg_id, m, compact=True)
+    return rec
+
+
+def pool(cfg_id: int, start: int, count: int, workers: int):
+    """Every realization of a BASELINE config through the reference, one per
+    worker process (the pattern of homogenize.py:149-161), compact records
+    with N_PROJ projections each -> config{cfg}_full.json."""
+    from concurrent.futures import ProcessPoolExecutor
+    path = os.path.join(HERE, f"config{cfg_id}_full.json")
+    recs = {}
+    if os.path.exists(path):
+        recs = {r["m"]: r for r in json.load(open(path))["records"]}
+    todo = [m for m in range(start, start + count) if m not in recs]
+    with ProcessPoolExecutor(max_workers=workers) as ex:
+        for rec in ex.map(_pool_one, [(cfg_id, m) for m in todo]):
+            recs[rec["m"]] = rec
+            print(cfg_id, rec["m"], rec["iterations"], round(rec["t_solve_s"], 1), flush=True)
+            with open(path + ".tmp", "w") as fh:
+                json.dump({"generator": "tests/golden/make_golden.py pool (reference checkerhom)",
+                           "numpy": np.__version__, "n_proj": N_PROJ, "proj_seed": PROJ_SEED,
+                           "records": [recs[k] for k in sorted(recs)]}, fh)
+            os.replace(path + ".tmp", path)
 
 
 def formats():
@@ -289,5 +337,7 @@ if __name__ == "__main__":
         small()
     elif sys.argv[1] == "formats":
         formats()
+    elif sys.argv[1] == "pool":
+        pool(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]))
     else:
         configs(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]))

@@ -72,7 +72,95 @@ def test_coefficient_grid_matches_reference():
     g = golden_small()
     cfg = chk.LatticeConfig(d=3, L=4, n0=4, alpha="1/4", lam=0.4)
     r = chk.sample_realization(cfg, 2)
-    assert np.allclose(chk.coefficient_grid(r), g["case1_coef"], rtol=0, atol=1e-15)
+    grid = chk.coefficient_grid(r)
+    assert isinstance(grid, chk.CoefficientGrid) and grid.n == cfg.n and grid.d == 3
+    assert np.allclose(grid.values, g["case1_coef"], rtol=0, atol=1e-15)
+
+
+def test_realization_reference_constructor():
+    """Realization(config, covered, cell_beta, seed) as in lattice.py:208-227, and
+    the lazily derived views agree with the dense sampler's."""
+    cfg = chk.LatticeConfig(d=3, L=4, n0=4, alpha="1/2", lam=0.2,
+                            contrast=chk.ContrastModel.two_value(0.3, 0.7))
+    r = chk.sample_realization(cfg, 5)
+    r2 = chk.Realization(cfg, r.covered, r.cell_beta, r.seed)
+    assert r2 == r and r2.num_covered == r.num_covered
+    assert np.array_equal(r2.beta_cells, r.beta_cells)
+    assert np.array_equal(r2.covered_mask, r.covered_mask)
+    assert r2.to_json() == r.to_json()
+    assert chk.Realization.coerce(r2) is r2
+    with pytest.raises(AttributeError):
+        r2.seed = 1
+    with pytest.raises(chk.ConfigurationError):
+        chk.Realization(cfg, {(0, 0, 0)}, {}, 1)
+    # duck-typed foreign realization (same fields as the reference's)
+    class Foreign:
+        config = cfg
+        covered = r.covered
+        cell_beta = r.cell_beta
+        seed = r.seed
+    assert chk.Realization.coerce(Foreign()) == r
+    assert np.array_equal(chk.coefficient_grid(Foreign()).values, chk.coefficient_grid(r).values)
+
+
+def test_spectral_api_matches_oracle():
+    """eigensum_tensor / pseudoinverse_diag / regularized_inverse_diag
+    (spectral.py:26-95) against the pinned oracle's diagonals."""
+    from oracle import checkerhom_oracle as orc
+    from paper_2007_06524_b200.spectral import _diag_kind
+
+    for n in (8, 16):
+        g = chk.eigensum_tensor(3, chk.fourier_eigenvalues(n))
+        assert g.value((1, 2, 3)) == pytest.approx(g.array()[1, 2, 3])
+        pinv = chk.pseudoinverse_diag(g)
+        assert np.array_equal(pinv.values, orc.pseudoinverse_diag(n))
+        reg = chk.regularized_inverse_diag(g, 1e-3)
+        assert np.allclose(reg.values, orc.pseudoinverse_diag(n, delta=1e-3), rtol=1e-15, atol=0)
+        assert chk.regularized_inverse_diag(g, 0.0).values is not None
+        assert _diag_kind(pinv) == ("fourier", 0.0)
+        assert _diag_kind(reg) == ("regularized", 1e-3)
+        # a foreign object carrying only (d, n, values), e.g. the reference's dataclass
+        Bare = type("Bare", (), {"d": 3, "n": n, "values": reg.values})
+        kind, delta = _diag_kind(Bare())
+        assert kind == "regularized" and delta == pytest.approx(1e-3, rel=1e-15)
+        Other = type("Other", (), {"d": 3, "n": n, "values": np.ones((n, n, n))})
+        with pytest.raises(ValueError):
+            _diag_kind(Other())
+    with pytest.raises(ValueError):
+        chk.eigensum_tensor(4, chk.fourier_eigenvalues(8))
+
+
+def test_philox_keys_are_the_reference_stream_keys():
+    """The keys the device sampler consumes are those of
+    Philox(SeedSequence(seed)) (lattice.py:279-281)."""
+    seeds = [chk.derive_seed(0, m) for m in range(4)]
+    keys = chk.philox_keys(seeds)
+    for s, k in zip(seeds, keys):
+        st = np.random.Philox(np.random.SeedSequence(s)).state
+        assert np.array_equal(st["state"]["key"], k)
+        assert not st["state"]["counter"].any() and st["buffer_pos"] == 4
+
+
+def test_philox4x64_restatement_matches_numpy():
+    """Pure-Python Philox4x64-10 with the counter / word mapping the CUDA sampler
+    uses (chk_sample.cuh) reproduces Generator(Philox).random()."""
+    M = (1 << 64) - 1
+
+    def block(ctr, key):
+        c = [ctr, 0, 0, 0]
+        k = list(key)
+        for r in range(10):
+            if r:
+                k = [(k[0] + 0x9E3779B97F4A7C15) & M, (k[1] + 0xBB67AE8584CAA73B) & M]
+            p0, p1 = 0xD2E7470EE14C6C93 * c[0], 0xCA5A826395121157 * c[2]
+            c = [(p1 >> 64) ^ c[1] ^ k[0], p1 & M, (p0 >> 64) ^ c[3] ^ k[1], p0 & M]
+        return c
+
+    seed = chk.derive_seed(0, 7)
+    key = [int(v) for v in chk.philox_keys([seed])[0]]
+    ref = np.random.Generator(np.random.Philox(np.random.SeedSequence(seed))).random(37)
+    mine = [(block(i // 4 + 1, key)[i % 4] >> 11) * (1.0 / 9007199254740992.0) for i in range(37)]
+    assert np.array_equal(ref, np.asarray(mine))
 
 
 @pytest.mark.parametrize("n", [8, 16, 32, 64, 128, 256, 512])
