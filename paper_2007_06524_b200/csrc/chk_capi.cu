@@ -1073,13 +1073,12 @@ int32_t chk_pcg_solve_seeds(const chk_grid* grid, const chk_precond_plan* plan, 
 
 int32_t chk_sample_cells(const chk_grid* grid, const uint64_t* keys, double coverage_prob, int32_t contrast_kind,
                          double beta0, double beta1, double* beta, int32_t B, void* stream) {
-  Geo g;
-  int rc = check_grid(grid, &g);
-  if (rc) return rc;
+  // only the lattice matters here (any L; no grid-size restriction of the solver)
+  if (!grid || grid->L < 1 || grid->d != 3) return fail(CHK_EINVAL, "bad grid (need d = 3, L >= 1)");
   if (!keys || !beta || B < 1) return fail(CHK_EINVAL, "bad arguments");
   if (contrast_kind != CHK_CONTRAST_FIXED && contrast_kind != CHK_CONTRAST_TWO_VALUE)
     return fail(CHK_EINVAL, "contrast_kind must be CHK_CONTRAST_FIXED or CHK_CONTRAST_TWO_VALUE");
-  const int ncell = g.L * g.L * g.L;
+  const int ncell = grid->L * grid->L * grid->L;
   const int gx = (int)std::min<long long>(((long long)ncell / 4 + 255) / 256 + 1, 1184);
   sample_cells_kernel<<<dim3(gx, B), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       keys, ncell, coverage_prob, contrast_kind, beta0, beta1, beta);
