@@ -568,7 +568,7 @@ def run_slab(args):
     comm = slab.TorchComm()
 
     def step():
-        return slab.slab_solve([R], comm)
+        return slab.slab_solve([R], comm, chunks=args.slab_chunks)
 
     for _ in range(args.warmup):
         res = step()
@@ -641,6 +641,8 @@ def main():
                     help="realizations per pipelined chunk of the host-buffer solve (default B/4)")
     ap.add_argument("--slab", action="store_true",
                     help="force the slab-decomposed path (default for config 5 when N > 1)")
+    ap.add_argument("--slab-chunks", type=int, default=4,
+                    help="plane chunks of the slab phases (exchange overlapped with the next chunk)")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU (gloo) run of the multi-rank harness with a stub solve (tests)")
     args = ap.parse_args()

@@ -224,6 +224,21 @@ int32_t chk_slab_phase(const chk_grid* grid, const chk_precond_plan* plan, const
                        void* xa, void* xb, const double* halo_lo, const double* halo_hi, double* red,
                        int32_t B, const chk_pcg_opts* opts, void* workspace, size_t workspace_bytes,
                        void* stream);
+/* The plane phases (FWD_INIT, FWD_Q, INV) over local planes [plane_begin,
+ * plane_begin + plane_count) only: a phase split into plane chunks lets the
+ * all_to_all of chunk k (rows of those planes, contiguous per destination in
+ * xa / xb) overlap the kernels of chunk k+1.  The chunks of one phase must run
+ * in plane order on one stream; plane_count < 0 means "to the last plane". */
+int32_t chk_slab_phase_planes(const chk_grid* grid, const chk_precond_plan* plan, const chk_slab* slab,
+                              int32_t phase, int32_t it, int32_t plane_begin, int32_t plane_count,
+                              const double* beta, const double* f, double* u, double* p, void* xa, void* xb,
+                              const double* halo_lo, const double* halo_hi, double* red, int32_t B,
+                              const chk_pcg_opts* opts, void* workspace, size_t workspace_bytes, void* stream);
+/* Stream-ordered copy of the B per-realization status words (3 = still active)
+ * into `status` ([B] int32, pinned host or device): the convergence poll without
+ * a host synchronisation. */
+int32_t chk_slab_status_async(const chk_grid* grid, const chk_slab* slab, int32_t B, int32_t max_iter,
+                              void* workspace, int32_t* status, void* stream);
 /* Per-realization status words (device -> host, synchronous on `stream`). */
 int32_t chk_slab_read_state(const chk_grid* grid, const chk_slab* slab, int32_t B, int32_t max_iter,
                             void* workspace, int32_t* iterations, double* final_rel, int32_t* status,

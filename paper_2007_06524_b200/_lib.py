@@ -64,6 +64,9 @@ SIGNATURES = {
     "chk_slab_workspace_bytes": (_sz, [_gp, _vp, _vp, _i32, _i32]),
     "chk_slab_phase": (_i32, [_gp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _i32, ctypes.POINTER(ChkPcgOpts), _vp, _sz, _vp]),
+    "chk_slab_phase_planes": (_i32, [_gp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                     _vp, _vp, _i32, ctypes.POINTER(ChkPcgOpts), _vp, _sz, _vp]),
+    "chk_slab_status_async": (_i32, [_gp, _vp, _i32, _i32, _vp, _vp, _vp]),
     "chk_slab_read_state": (_i32, [_gp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 

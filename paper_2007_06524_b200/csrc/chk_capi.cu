@@ -161,10 +161,10 @@ struct Ops {
   }
   static int maxblk() { return PLANE_BLOCKS > TILES ? PLANE_BLOCKS : TILES; }
   // single-GPU layout: all planes, one column chunk, periodic halo inside p
-  static SlabGeo whole() { return SlabGeo{N, 0, 1, NR * H, 0, TILES, nullptr, nullptr}; }
+  static SlabGeo whole() { return SlabGeo{N, 0, 1, NR * H, 0, TILES, nullptr, nullptr, 0, N}; }
   // rank `rank` of `P` owning n/P consecutive planes and column chunk `rank`
   static SlabGeo slab(int P, int rank, const double* lo, const double* hi) {
-    return SlabGeo{N / P, rank * (N / P), P, NR * H / P, rank * (TILES / P), TILES / P, lo, hi};
+    return SlabGeo{N / P, rank * (N / P), P, NR * H / P, rank * (TILES / P), TILES / P, lo, hi, 0, N / P};
   }
   static bool slab_ok(int P) { return P >= 1 && N % P == 0 && (N / P) >= 1 && TILES % P == 0 && P <= 64; }
 
@@ -198,7 +198,7 @@ struct Ops {
   static int fwd(int mode, cudaStream_t s, int B, Geo g, const double* beta, const double* src,
                  double* u, double2* S, PlanDev pl, SolveCtl ctl, int it, SlabGeo sg = whole()) {
     const size_t sm = plane_smem();
-    dim3 grid(B * sg.nloc * G);
+    dim3 grid(B * sg.nrun * G);
     ProfScope ps(1, s);
     if (mode == FWD_APPLY) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_APPLY, false>, sm));
@@ -280,7 +280,7 @@ struct Ops {
   static int inv(int mode, cudaStream_t s, int B, const double2* S, double* out, double* u,
                  PlanDev pl, SolveCtl ctl, int it, SlabGeo sg = whole()) {
     const size_t sm = plane_smem();
-    dim3 grid(B * sg.nloc * G);
+    dim3 grid(B * sg.nrun * G);
     ProfScope ps(3, s);
     if (mode == INV_APPLY) {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_APPLY>, sm));
@@ -1143,12 +1143,29 @@ int32_t chk_slab_phase(const chk_grid* grid, const chk_precond_plan* plan, const
                        void* xa, void* xb, const double* halo_lo, const double* halo_hi, double* red,
                        int32_t B, const chk_pcg_opts* opts, void* workspace, size_t workspace_bytes,
                        void* stream) {
+  return chk_slab_phase_planes(grid, plan, slab, phase, it, 0, -1, beta, f, u, p, xa, xb, halo_lo, halo_hi, red,
+                               B, opts, workspace, workspace_bytes, stream);
+}
+
+int32_t chk_slab_phase_planes(const chk_grid* grid, const chk_precond_plan* plan, const chk_slab* slab,
+                              int32_t phase, int32_t it, int32_t plane_begin, int32_t plane_count,
+                              const double* beta, const double* f, double* u, double* p, void* xa, void* xb,
+                              const double* halo_lo, const double* halo_hi, double* red, int32_t B,
+                              const chk_pcg_opts* opts, void* workspace, size_t workspace_bytes, void* stream) {
   Geo g;
   int rc = check_grid(grid, &g);
   if (rc) return rc;
   if (!plan || plan->n != grid->n || !opts || B < 1 || !red) return fail(CHK_EINVAL, "bad arguments");
   SlabGeo sg;
   if ((rc = slab_geo(grid, slab, halo_lo, halo_hi, &sg))) return rc;
+  if (plane_count < 0) plane_count = sg.nloc - plane_begin;
+  if (plane_begin < 0 || plane_count < 1 || plane_begin + plane_count > sg.nloc)
+    return fail(CHK_EINVAL, "plane range outside the rank's slab");
+  const bool ranged = plane_begin != 0 || plane_count != sg.nloc;
+  if (ranged && phase != CHK_SLAB_FWD_INIT && phase != CHK_SLAB_FWD_Q && phase != CHK_SLAB_INV)
+    return fail(CHK_EINVAL, "only the plane phases (FWD_INIT, FWD_Q, INV) take a plane range");
+  sg.run0 = plane_begin;
+  sg.nrun = plane_count;
   const int n = grid->n;
   SlabWs w = slab_carve(workspace, n, slab->nranks, B, opts->max_iter);
   if (!workspace || workspace_bytes < w.bytes) return fail(CHK_EINVAL, "workspace too small");
@@ -1182,7 +1199,7 @@ int32_t chk_slab_phase(const chk_grid* grid, const chk_precond_plan* plan, const
       case CHK_SLAB_MID_DECIDE: rc = decide(DECIDE_MID); break;
       case CHK_SLAB_INV: rc = O::inv(it == 0 ? INV_INIT : INV_ITER, s, B, XA, p, u, pl, ctl, it, sg); break;
       case CHK_SLAB_FWD_Q:
-        CHK_CUDA(zero_red());
+        if (plane_begin == 0) CHK_CUDA(zero_red());  // first plane chunk of the phase
         rc = O::fwd(FWD_Q, s, B, g, beta, p, u, XA, pl, ctl, it, sg);
         break;
       case CHK_SLAB_ALPHA_DECIDE: rc = decide(DECIDE_ALPHA); break;
@@ -1201,6 +1218,17 @@ int32_t chk_slab_phase(const chk_grid* grid, const chk_precond_plan* plan, const
     }
   });
   return rc;
+}
+
+int32_t chk_slab_status_async(const chk_grid* grid, const chk_slab* slab, int32_t B, int32_t max_iter,
+                              void* workspace, int32_t* status, void* stream) {
+  if (!grid || !slab || !workspace || !status || B < 1 || max_iter < 1 || !supported_n(grid->n))
+    return fail(CHK_EINVAL, "bad arguments");
+  SlabWs w = slab_carve(workspace, grid->n, slab->nranks, B, max_iter);
+  // the status word of each RState, strided, into a dense [B] int32 array (pinned host or device)
+  CHK_CUDA(cudaMemcpy2DAsync(status, sizeof(int32_t), &w.st->status, sizeof(RState), sizeof(int32_t), B,
+                             cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return CHK_OK;
 }
 
 int32_t chk_slab_read_state(const chk_grid* grid, const chk_slab* slab, int32_t B, int32_t max_iter,

@@ -94,6 +94,8 @@ struct SlabGeo {
   int tiles;
   const double* halo_lo;  // [B][n*n] plane x0_off-1, null -> periodic inside p
   const double* halo_hi;  // [B][n*n] plane x0_off+nloc, null -> periodic inside p
+  int run0;               // plane passes: launch covers local planes [run0, run0 + nrun)
+  int nrun;               // (a slab phase split into plane chunks overlapped with the exchange)
 };
 
 // Interleaved spectrum layout (n >= 256): a plane chunk is stored [ncols/W][G][W]
@@ -870,10 +872,11 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   constexpr int HP = H;
   extern __shared__ double2 buf[];
   __shared__ double scratch[64];
-  const int nlg = sg.nloc * G;
-  const int b = bid / nlg;
-  const int rem = bid - b * nlg;
-  const int x0l = rem / G, gg = rem - (rem / G) * G;  // local plane, x1 group
+  const int nlg = sg.nloc * G;                        // CTAs per realization (all planes)
+  const int b = bid / (sg.nrun * G);
+  const int rrun = bid - b * (sg.nrun * G);
+  const int x0l = sg.run0 + rrun / G, gg = rrun - (rrun / G) * G;  // local plane, x1 group
+  const int rem = x0l * G + gg;                       // partial slot of this CTA
   const int x0 = sg.x0_off + x0l;                     // global plane
   const size_t nn = (size_t)N * N;
   const size_t nb = (size_t)sg.nloc * nn;             // local DOF per realization
@@ -1872,10 +1875,9 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
   constexpr int HP = H;
   extern __shared__ double2 buf[];
   __shared__ alignas(8) uint64_t bar;
-  const int nlg = sg.nloc * G;
-  const int b = bid / nlg;
-  const int rem = bid - b * nlg;
-  const int x0 = rem / G, gg = rem - (rem / G) * G;  // local plane, x1 group
+  const int b = bid / (sg.nrun * G);
+  const int rrun = bid - b * (sg.nrun * G);
+  const int x0 = sg.run0 + rrun / G, gg = rrun - (rrun / G) * G;  // local plane, x1 group
   const size_t nb = (size_t)sg.nloc * N * N;
   double alpha = 0.0, beta = 0.0;
   bool do_p = true, do_u = false;

@@ -13,7 +13,13 @@ PCG iteration (pcg_solve, solver.py:161-185):
 
 The collectives run between kernel launches on the caller's stream
 (torch.distributed over NCCL: NVLink/NVSwitch on one node); every rank takes
-the same decisions from bit-identical allreduced scalars.  ``LocalComm``
+the same decisions from bit-identical allreduced scalars.  With ``chunks`` > 1
+the plane phases run in plane chunks and each all_to_all is split the same
+way: the exchange of chunk k (asynchronous NCCL work on its own stream) runs
+under the FWD kernels of chunk k+1, and the return exchange of chunk k+1 under
+the INV kernels of chunk k; the halo of p travels under the interior planes.
+The convergence poll is a stream-ordered copy of the status words into pinned
+memory checked one poll later (no host synchronisation on the iteration).  ``LocalComm``
 executes the same schedule for P virtual ranks inside one process (explicit
 device copies between phases, no kernel ever waits on another) -- this is how
 the decomposition is verified on a single GPU.
@@ -59,21 +65,50 @@ class TorchComm:
         (out,), (inp,) = outs, ins
         self.dist.all_to_all_single(out, inp, group=self.group)
 
-    def halo(self, firsts, lasts, los, his):
+    def all_to_all_planes(self, outs, ins, shape, p0, p1):
+        """Exchange of the rows of local planes [p0, p1) only (buffers viewed as
+        [P][B][nloc][row]; each (destination, realization) block is contiguous):
+        grouped point-to-point sends / receives (ncclSend / ncclRecv under one
+        group on NCCL), asynchronous -- returns the pending requests (finish()
+        makes the current stream wait for them)."""
+        (out,), (inp,) = outs, ins
+        dist, P, r = self.dist, self.P, self.rank
+        o = out.view(shape)[:, :, p0:p1]
+        i = inp.view(shape)[:, :, p0:p1]
+        o[r].copy_(i[r])
+        ops = []
+        for k in range(1, P):
+            dst, src = (r + k) % P, (r - k) % P
+            for b in range(shape[1]):
+                ops.append(dist.P2POp(dist.isend, i[dst, b], dst, self.group))
+                ops.append(dist.P2POp(dist.irecv, o[src, b], src, self.group))
+        return (dist.batch_isend_irecv(ops) if ops else []), None
+
+    def finish(self, pending):
+        works, unpack = pending
+        for w in works:
+            w.wait()
+        if unpack is not None:
+            unpack[0].copy_(unpack[1])
+
+    def halo(self, firsts, lasts, los, his, async_op=False):
         """lo[r] <- last plane of rank r-1, hi[r] <- first plane of rank r+1 (periodic)."""
         (first,), (last,), (lo,), (hi,) = firsts, lasts, los, his
         P, r = self.P, self.rank
         if P == 1:
             lo.copy_(last)
             hi.copy_(first)
-            return
+            return ([], None) if async_op else None
         dist = self.dist
         prv, nxt = (r - 1) % P, (r + 1) % P
         ops = [dist.P2POp(dist.isend, last.contiguous(), nxt, self.group),
                dist.P2POp(dist.irecv, lo, prv, self.group),
                dist.P2POp(dist.isend, first.contiguous(), prv, self.group),
                dist.P2POp(dist.irecv, hi, nxt, self.group)]
-        for req in dist.batch_isend_irecv(ops):
+        reqs = dist.batch_isend_irecv(ops)
+        if async_op:
+            return reqs, None
+        for req in reqs:
             req.wait()
 
 
@@ -97,11 +132,23 @@ class LocalComm:
             for s in range(P):
                 outs[s].view(P, -1)[r].copy_(src[s])
 
-    def halo(self, firsts, lasts, los, his):
+    def all_to_all_planes(self, outs, ins, shape, p0, p1):
+        P = self.P
+        for r in range(P):
+            src = ins[r].view(shape)
+            for s in range(P):
+                outs[s].view(shape)[r, :, p0:p1].copy_(src[s, :, p0:p1])
+        return [], None
+
+    def finish(self, pending):
+        pass
+
+    def halo(self, firsts, lasts, los, his, async_op=False):
         P = self.P
         for r in range(P):
             los[r].copy_(lasts[(r - 1) % P])
             his[r].copy_(firsts[(r + 1) % P])
+        return ([], None) if async_op else None
 
 
 # ----------------------------------------------------------------------------
@@ -153,10 +200,21 @@ class SlabRank:
         v = self.p.view(self.B, self.nloc, self.n * self.n)
         return v[:, 0].contiguous(), v[:, self.nloc - 1].contiguous()
 
-    def phase(self, ph: int, it: int = 0):
+    def xshape(self):
+        """Exchange buffers as [P][B][nloc][row] float64 views."""
+        return (self.P, self.B, self.nloc, -1)
+
+    def status_async(self, out):
+        """Stream-ordered copy of the B status words into ``out`` (pinned int32)."""
+        _lib.check(self.lib.chk_slab_status_async(
+            ctypes.byref(self.grid), ctypes.byref(self.slab), self.B, self.opts.max_iter,
+            ctypes.c_void_p(self.ws.data_ptr()), ctypes.c_void_p(out.data_ptr()), _lib.stream_handle()))
+
+    def phase(self, ph: int, it: int = 0, planes=None):
         vp = ctypes.c_void_p
-        rc = self.lib.chk_slab_phase(
-            ctypes.byref(self.grid), self.plan.handle, ctypes.byref(self.slab), ph, it,
+        p0, cnt = planes if planes is not None else (0, -1)
+        rc = self.lib.chk_slab_phase_planes(
+            ctypes.byref(self.grid), self.plan.handle, ctypes.byref(self.slab), ph, it, int(p0), int(cnt),
             vp(self.beta.data_ptr()), vp(self.f.data_ptr()), vp(self.u.data_ptr()), vp(self.p.data_ptr()),
             vp(self.xa.data_ptr()), vp(self.xb.data_ptr()), vp(self.halo_lo.data_ptr()),
             vp(self.halo_hi.data_ptr()), vp(self.red.data_ptr()), self.B, ctypes.byref(self.copts),
@@ -178,46 +236,110 @@ class SlabRank:
         return its, fin, st, proj, hist
 
 
-def slab_solve(ranks: list, comm, poll_every: int = 2) -> BatchResult:
+def plane_chunks(nloc: int, chunks: int) -> list:
+    """Plane ranges of a chunked plane phase: the interior planes [1, nloc-1) in
+    ``chunks`` pieces first (they need no halo), then the two edge planes."""
+    if chunks <= 1 or nloc < 4:
+        return [(0, nloc)]
+    inner = nloc - 2
+    k = min(chunks, inner)
+    cuts = [1 + (inner * j) // k for j in range(k + 1)]
+    return [(cuts[j], cuts[j + 1]) for j in range(k)] + [(0, 1), (nloc - 1, nloc)]
+
+
+def slab_solve(ranks: list, comm, poll_every: int = 2, chunks: int = 1) -> BatchResult:
     """Run the batched PCG over the ranks held by this process (all P for
     LocalComm, one for TorchComm).  Returns rank-local u in ``result.u``
-    (list of [B, nloc*n*n] tensors) and the (rank-identical) reports."""
-    opts = ranks[0].opts
+    (list of [B, nloc*n*n] tensors) and the (rank-identical) reports.
 
-    def each(ph, it=0):
+    chunks > 1: plane phases and their all_to_all exchanges in plane chunks
+    (overlapped with NCCL); the convergence poll is asynchronous (one poll of
+    look-ahead), so the host never waits on the current iteration."""
+    torch = ranks[0].torch
+    opts = ranks[0].opts
+    shape = ranks[0].xshape()
+    pieces = plane_chunks(ranks[0].nloc, chunks)
+
+    def each(ph, it=0, planes=None):
         for r in ranks:
-            r.phase(ph, it)
+            r.phase(ph, it, planes)
 
     def reds():
         comm.allreduce([r.red for r in ranks])
 
+    def forward(ph, it):
+        """plane phase ph (FWD_INIT / FWD_Q) then exchange x0 slabs -> column chunks"""
+        if len(pieces) == 1:
+            each(ph, it)
+            return [("all", None)]
+        pend = []
+        for (p0, p1) in pieces:
+            if p0 == 0 and halo_pending[0] is not None:
+                comm.finish(halo_pending[0])
+                halo_pending[0] = None
+            each(ph, it, (p0, p1 - p0))
+            pend.append(comm.all_to_all_planes([r.xb for r in ranks], [r.xa for r in ranks], shape, p0, p1))
+        return pend
+
+    def after_forward(pend):
+        if pend and pend[0][0] == "all":
+            comm.all_to_all([r.xb for r in ranks], [r.xa for r in ranks])
+            return
+        for pd in pend:
+            comm.finish(pd)
+
+    def backward(it):
+        """exchange column chunks -> x0 slabs, then INV, chunk by chunk"""
+        if len(pieces) == 1:
+            comm.all_to_all([r.xa for r in ranks], [r.xb for r in ranks])
+            each(INV, it)
+            return
+        pend = [comm.all_to_all_planes([r.xa for r in ranks], [r.xb for r in ranks], shape, p0, p1)
+                for (p0, p1) in pieces]
+        for (p0, p1), pd in zip(pieces, pend):
+            comm.finish(pd)
+            each(INV, it, (p0, p1 - p0))
+
+    halo_pending = [None]
     each(STATS)
     reds()
     each(STATS_DECIDE)
-    each(FWD_INIT)
-    comm.all_to_all([r.xb for r in ranks], [r.xa for r in ranks])
+    after_forward(forward(FWD_INIT, 0))
     each(MID, 0)
     reds()
     each(MID_DECIDE, 0)
-    comm.all_to_all([r.xa for r in ranks], [r.xb for r in ranks])
-    each(INV, 0)
+    backward(0)
+    # asynchronous convergence poll: status words -> pinned host every poll_every
+    # iterations, read one poll later
+    stat = [torch.empty(ranks[0].B, dtype=torch.int32).pin_memory() for _ in range(2)]
+    evs = [torch.cuda.Event(), torch.cuda.Event()]
+    npoll = 0
     for it in range(1, opts.max_iter + 1):
         pl = [r.planes() for r in ranks]
-        comm.halo([f for f, _ in pl], [l for _, l in pl], [r.halo_lo for r in ranks],
-                  [r.halo_hi for r in ranks])
-        each(FWD_Q, it)
+        halo = comm.halo([f for f, _ in pl], [l for _, l in pl], [r.halo_lo for r in ranks],
+                         [r.halo_hi for r in ranks], async_op=True)
+        if len(pieces) == 1:
+            comm.finish(halo)
+        else:
+            halo_pending[0] = halo
+        pend = forward(FWD_Q, it)
         reds()
         each(ALPHA_DECIDE, it)
-        comm.all_to_all([r.xb for r in ranks], [r.xa for r in ranks])
+        after_forward(pend)
         each(MID, it)
         reds()
         each(MID_DECIDE, it)
-        comm.all_to_all([r.xa for r in ranks], [r.xb for r in ranks])
-        each(INV, it)
+        backward(it)
         if it % poll_every == 0 or it == opts.max_iter:
-            _, _, st, _, _ = ranks[0].read_state()
-            if not np.any(st == 3):  # every rank holds the same status words
-                break
+            if npoll > 0:
+                prev = (npoll - 1) & 1
+                evs[prev].synchronize()
+                if not np.any(stat[prev].numpy() == 3):  # every rank holds the same status words
+                    break
+            cur = npoll & 1
+            ranks[0].status_async(stat[cur])
+            evs[cur].record()
+            npoll += 1
     each(MEANU)
     reds()
     each(MEANU_APPLY)

@@ -33,27 +33,34 @@ def _problem(cfg_id, ms):
     return cfg, beta, A, F, opts
 
 
-def _slab(cfg, beta, F, opts, P):
+def _slab(cfg, beta, F, opts, P, chunks=1):
     n = cfg.n
     nloc = n // P
     Fv = F.reshape(F.shape[0], n, n * n)
     ranks = [slab.SlabRank(cfg, beta, Fv[:, r * nloc:(r + 1) * nloc].contiguous(), P, r, opts)
              for r in range(P)]
-    res = slab.slab_solve(ranks, slab.LocalComm(P))
+    res = slab.slab_solve(ranks, slab.LocalComm(P), chunks=chunks)
     u = torch.cat([x.reshape(F.shape[0], nloc, n * n) for x in res.u], dim=1).reshape(F.shape[0], -1)
     return res, u
 
 
-@pytest.mark.parametrize("cfg_id,ms,P", [(2, [0, 1, 2], 2), (2, [3], 4), (3, [0, 1], 8), (4, [0], 2)])
-def test_slab_matches_single_gpu(cfg_id, ms, P):
+@pytest.mark.parametrize("cfg_id,ms,P,chunks", [(2, [0, 1, 2], 2, 1), (2, [3], 4, 1), (3, [0, 1], 8, 1),
+                                                (4, [0], 2, 1), (2, [0, 1], 2, 3), (3, [4], 4, 4), (4, [1], 4, 2)])
+def test_slab_matches_single_gpu(cfg_id, ms, P, chunks):
+    """The slab schedule (P virtual ranks) reproduces the single-GPU solver; with
+    chunks > 1 the plane phases and exchanges run in plane chunks (interior
+    planes first, then the two halo-dependent edge planes)."""
     cfg, beta, A, F, opts = _problem(cfg_id, ms)
     ref = chk.pcg_solve_batched(A, F, opts)
-    res, u = _slab(cfg, beta, F, opts, P)
+    res, u = _slab(cfg, beta, F, opts, P, chunks)
     assert list(res.iterations) == list(ref.iterations)
     assert np.all(res.status == 0)
     for j in range(len(ms)):
         its = int(ref.iterations[j])
-        assert np.allclose(res.history[j, :its], ref.history[j, :its], rtol=1e-9, atol=0)
+        # the rank-local partial sums are allreduced, so p.Ap and the Parseval sums are
+        # added in another order than on one GPU: roundoff-level, but it grows relative
+        # to the residual as the residual falls (config 4 reaches 6e-11 ||f||)
+        assert np.allclose(res.history[j, :its], ref.history[j, :its], rtol=1e-7, atol=0)
         rel = float(torch.linalg.norm(u[j] - ref.u[j]) / torch.linalg.norm(ref.u[j]))
         assert rel <= 1e-10, rel
 
@@ -66,7 +73,7 @@ def test_slab_config5_n512_vs_reference():
         pytest.skip("config 5 golden not generated")
     rec = recs[0]
     cfg, beta, A, F, opts = _problem(5, [0])
-    res, u = _slab(cfg, beta, F, opts, 2)
+    res, u = _slab(cfg, beta, F, opts, 2, chunks=4)
     assert int(res.iterations[0]) == rec["iterations"]
     its = rec["iterations"]
     assert np.allclose(res.history[0, :its], rec["residuals"], rtol=1e-7, atol=0)
