@@ -20,6 +20,8 @@
 // decisions (alpha, breakdown, stop, beta) -- or, when one grid is
 // slab-decomposed over GPUs, publishes rank-local sums for an allreduce.
 #pragma once
+#include <type_traits>
+
 #include "chk_fft.cuh"
 #include "chk_tma.cuh"
 
@@ -28,6 +30,9 @@
 #endif
 #ifndef CHK_FWD_PF  // L2 prefetch of the CTA's own p rows at the start of the forward pass
 #define CHK_FWD_PF 1
+#endif
+#ifndef CHK_FWD_CS  // n = 256 plane passes: CTA-uniform cell-row de-duplication + half-row halo shuffles
+#define CHK_FWD_CS 1
 #endif
 #ifndef CHK_INV_PF  // L2 prefetch of the p / u rows at the start of the inverse pass (n <= 128;
 #define CHK_INV_PF 1    // at n >= 256 the prefetched rows are evicted before use: +38 % DRAM reads)
@@ -55,7 +60,7 @@ struct RState {
   int status;
   int iters;
   int rhs_projected;
-  int pad0;
+  int done;          // early-download finalisation ran (host pipeline), 0 otherwise
   double normf;      // ||f|| after the optional mean projection (solver.py:132,142)
   double norm_pf;    // sqrt|r0.z0| (solver.py:156)
   double mean_f;     // mean removed from f when projected
@@ -514,7 +519,13 @@ __device__ __forceinline__ void cell4(const double* b00, const double* b01, cons
   v00 = s0 ? v10 : (s1 ? v01 : __ldg(b00 + c));
 }
 
-template <int N, bool DEDUP = false>
+// CS (compile-time, n >= 256 plane passes): the caller knows per CTA that the x0 - 1
+// and x0 cell planes coincide (bit 0) / the x1 - 1 and x1 cell rows coincide
+// (bit 1), so those cell rows are loaded once (same values, same bits); CS = -1:
+// decide at run time (DEDUP) or not at all.  HALF: the 32 lanes of a warp hold 32
+// consecutive quads of one row (n >= 256), so the x2 halo comes from the
+// neighbouring lane by shuffle except at the two ends of the warp.
+template <int N, bool DEDUP = false, int CS = -1, bool HALF = false>
 __device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
                                                const double* __restrict__ beta, int x0, int x1,
                                                int x2s, double (&pc)[4], double (&q)[4]) {
@@ -535,6 +546,12 @@ __device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
   if constexpr (SHFL) {
     pl = __shfl_sync(0xffffffffu, pc[3], (threadIdx.x - 1) & (Q4 - 1), Q4);
     prr = __shfl_sync(0xffffffffu, pc[0], (threadIdx.x + 1) & (Q4 - 1), Q4);
+  } else if constexpr (HALF) {
+    const int lane = threadIdx.x & 31;
+    pl = __shfl_sync(0xffffffffu, pc[3], (lane - 1) & 31);
+    prr = __shfl_sync(0xffffffffu, pc[0], (lane + 1) & 31);
+    if (lane == 0) pl = __ldg(P3.c + row + ((x2s - 1) & nm));
+    if (lane == 31) prr = __ldg(P3.c + row + ((x2s + 4) & nm));
   } else {
     pl = __ldg(P3.c + row + ((x2s - 1) & nm));
     prr = __ldg(P3.c + row + ((x2s + 4) & nm));
@@ -550,7 +567,8 @@ __device__ __forceinline__ void stencil4_allin(const Geo& g, const Planes& P3,
   const double* b11 = beta + ((size_t)c00 * L + c10) * L;  // (x0,   x1)
   // DEDUP: coinciding cell rows loaded once (fewer loads, more live registers:
   // pays in the stand-alone stencil, not inside the register-bound plane passes)
-  const bool s0 = DEDUP && (c0m == c00), s1 = DEDUP && (c1m == c10);
+  const bool s0 = (CS >= 0) ? (CS & 1) != 0 : (DEDUP && (c0m == c00));
+  const bool s1 = (CS >= 0) ? (CS & 2) != 0 : (DEDUP && (c1m == c10));
   double m00, m01, m10, m11, z00, z01, z10, z11;
   cell4(b00, b01, b10, b11, s0, s1, cm, m00, m01, m10, m11);
   cell4(b00, b01, b10, b11, s0, s1, cc, z00, z01, z10, z11);
@@ -931,6 +949,26 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
         stencil_march<N, G, NR, false, false, false, true>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
       else
         stencil_march<N, G, NR, false, false>(g, P3, bb, x0, gg, sm, 2 * HP, acc);
+    } else if constexpr (ALLIN && Q4 == 64 && CHK_FWD_CS) {
+      // G >= n0: every row x1 = gg + G t of this CTA has the same x1 mod n0, so whether
+      // the x1 - 1 cell row coincides is CTA-uniform, as is the x0 - 1 cell plane
+      // (x0 fixed): four compile-time variants with the coinciding rows loaded once
+      const bool u0 = ((((x0 - 1) & (N - 1)) >> g.sh) == (x0 >> g.sh));
+      const bool u1 = (G >= g.mask + 1) && ((gg & g.mask) != 0);
+      auto body = [&](auto cs_tag) {
+        constexpr int CS = decltype(cs_tag)::value;
+        for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
+          const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
+          double pc[4], q[4];
+          stencil4_allin<N, false, CS, true>(g, P3, bb, x0, gg + G * t, x2, pc, q);
+          st_quad_smem(sm + t * 2 * HP, x2, q);
+          acc += ((pc[0] * q[0] + pc[1] * q[1]) + pc[2] * q[2]) + pc[3] * q[3];
+        }
+      };
+      if (u0 && u1) body(std::integral_constant<int, 3>{});
+      else if (u0) body(std::integral_constant<int, 1>{});
+      else if (u1) body(std::integral_constant<int, 2>{});
+      else body(std::integral_constant<int, 0>{});
     } else {
       for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
         const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
@@ -2026,6 +2064,7 @@ __global__ void __launch_bounds__(256) mean_u_kernel(const double* __restrict__ 
   const int x0 = rem / G, gg = rem - (rem / G) * G;
   const size_t nb = (size_t)sg.nloc * N * N;
   RState* st = ctl.st + b;
+  if (st->done) return;  // finalised early (its projection already applied)
   double s = 0.0;
   for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
     const int t = i / N, x2 = i - (i / N) * N;
@@ -2041,14 +2080,18 @@ __global__ void __launch_bounds__(256) mean_u_kernel(const double* __restrict__ 
   }
 }
 
-__global__ void __launch_bounds__(256) sub_mean_kernel(double* __restrict__ u, const RState* st,
-                                                       size_t nb, int B) {
+// mark: the early-download finalisation of one realization (sets RState.done so
+// the batch-wide projection at the end skips it)
+__global__ void __launch_bounds__(256) sub_mean_kernel(double* __restrict__ u, RState* st,
+                                                       size_t nb, int B, int mark) {
   const size_t total = nb * (size_t)B;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const int b = (int)(i / nb);
+    if (!mark && st[b].done) continue;
     u[i] -= st[b].mean_u;  // solver.py:169 (applied once: proj is linear and idempotent)
   }
+  if (mark && blockIdx.x == 0 && threadIdx.x == 0) st[0].done = 1;
 }
 
 // Slab mode: decisions from the allreduced sums red[B][4] (identical on every
