@@ -325,11 +325,6 @@ struct Ops {
     CHK_LAUNCHED();
     return CHK_OK;
   }
-  // per-realization mean of u for ONE realization (ctl offset to it): the early download
-  static void mean_u_launch(cudaStream_t s, const double* u, SolveCtl ctl) {
-    const SlabGeo sg = whole();
-    mean_u_kernel<N, G><<<sg.nloc * G, 256, 0, s>>>(u, ctl, sg);
-  }
   static int mean_u(cudaStream_t s, int B, const double* u, SolveCtl ctl, SlabGeo sg = whole()) {
     mean_u_kernel<N, G><<<B * sg.nloc * G, 256, 0, s>>>(u, ctl, sg);
     CHK_LAUNCHED();
@@ -721,26 +716,10 @@ size_t chk_pcg_workspace_bytes(const chk_grid* grid, const chk_precond_plan* pla
 
 namespace {
 
-// Early download of finished realizations (host pipeline): a realization whose
-// status left ACTIVE (seen by the convergence poll, so its last u update is
-// already queued) gets its mean projection (mean_u + sub_mean for that
-// realization alone -- the same per-realization reduction as the batch-wide
-// one) and the D2H copy of u on a copy stream while the rest of the batch
-// iterates; the batch-wide projection at the end skips it (RState.done).
-struct EagerDownload {
-  double* u_host = nullptr;  // [B][n^3] pinned host, or null (off)
-  cudaStream_t cs = nullptr;
-  std::vector<char> done;
-  std::vector<cudaEvent_t> events;
-  ~EagerDownload() {
-    for (auto e : events) cudaEventDestroy(e);
-  }
-};
-
 int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const double* beta, const double* f,
                        double* u, int32_t B, const chk_pcg_opts* opts, int32_t* iterations, double* final_rel,
                        int32_t* status, int32_t* rhs_projected, double* history, void* workspace,
-                       size_t workspace_bytes, void* stream, EagerDownload* eager) {
+                       size_t workspace_bytes, void* stream) {
   g_launches = 0;
   Geo g;
   int rc = check_grid(grid, &g);
@@ -765,8 +744,6 @@ int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const
   cudaEvent_t ev[2];
   CHK_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
   CHK_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-  const size_t nbv = (size_t)n * n * n;
-  if (eager) eager->done.assign(B, 0);
   auto run = [&]() -> int {
     int rc2 = CHK_OK;
     CHK_DISPATCH(n, {
@@ -789,34 +766,6 @@ int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const
             const RState* prev = hst_all + (size_t)(ev_i ^ 1) * B;
             bool any = false;
             for (int b = 0; b < B; ++b) any |= (prev[b].status == ST_ACTIVE);
-            if (eager && any) {  // (when none is active the batch-wide tail below is cheaper)
-              int nnew = 0;
-              for (int b = 0; b < B; ++b) {
-                if (prev[b].status == ST_ACTIVE || eager->done[b]) continue;
-                eager->done[b] = 1;
-                ++nnew;
-                SolveCtl cb = ctl;
-                cb.st += b;
-                cb.part += (size_t)2 * ctl.maxblk * b;
-                double* ub = u + nbv * b;
-                O::mean_u_launch(s, ub, cb);
-                sub_mean_kernel<<<148, 256, 0, s>>>(ub, w.st + b, nbv, 1, 1);
-                CHK_LAUNCHED();
-              }
-              if (nnew) {
-                cudaEvent_t e;
-                CHK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-                eager->events.push_back(e);
-                CHK_CUDA(cudaEventRecord(e, s));
-                CHK_CUDA(cudaStreamWaitEvent(eager->cs, e, 0));
-                for (int b = 0; b < B; ++b) {
-                  if (eager->done[b] != 1) continue;
-                  eager->done[b] = 2;  // queued
-                  CHK_CUDA(cudaMemcpyAsync(eager->u_host + nbv * b, u + nbv * b, sizeof(double) * nbv,
-                                           cudaMemcpyDeviceToHost, eager->cs));
-                }
-              }
-            }
             if (!any) {
               stop = true;
               return CHK_OK;
@@ -888,7 +837,7 @@ int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const
     });
     {
       const size_t nb = (size_t)n * n * n;
-      sub_mean_kernel<<<1184, 256, 0, s>>>(u, w.st, nb, B, 0);
+      sub_mean_kernel<<<1184, 256, 0, s>>>(u, w.st, nb, B);
       CHK_LAUNCHED();
     }
     return rc2;
@@ -897,26 +846,6 @@ int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
   if (rc) return rc;
-  if (eager) {  // the rest of the batch (projected by the batch-wide tail): contiguous runs
-    cudaEvent_t e;
-    CHK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    eager->events.push_back(e);
-    CHK_CUDA(cudaEventRecord(e, s));
-    CHK_CUDA(cudaStreamWaitEvent(eager->cs, e, 0));
-    for (int b = 0; b < B;) {
-      if (eager->done[b]) {
-        ++b;
-        continue;
-      }
-      int b1 = b;
-      while (b1 < B && !eager->done[b1]) ++b1;
-      CHK_CUDA(cudaMemcpyAsync(eager->u_host + nbv * b, u + nbv * b, sizeof(double) * nbv * (b1 - b),
-                               cudaMemcpyDeviceToHost, eager->cs));
-      b = b1;
-    }
-    CHK_CUDA(cudaEventRecord(e, eager->cs));
-    CHK_CUDA(cudaStreamWaitEvent(s, e, 0));  // the call's stream sees u on the host
-  }
   CHK_CUDA(cudaMemcpyAsync(hst, w.st, sizeof(RState) * B, cudaMemcpyDeviceToHost, s));
   if (history)
     CHK_CUDA(cudaMemcpyAsync(history, w.hist, sizeof(double) * (size_t)opts->max_iter * B,
@@ -944,7 +873,7 @@ int32_t chk_pcg_solve_batched(const chk_grid* grid, const chk_precond_plan* plan
                               int32_t* status, int32_t* rhs_projected, double* history,
                               void* workspace, size_t workspace_bytes, void* stream) {
   return solve_batched_impl(grid, plan, beta, f, u, B, opts, iterations, final_rel, status, rhs_projected, history,
-                            workspace, workspace_bytes, stream, nullptr);
+                            workspace, workspace_bytes, stream);
 }
 
 // Host-buffer pipeline: three lanes (host threads, each with its own stream,
@@ -1025,13 +954,9 @@ int host_pipeline(const chk_grid* grid, const chk_precond_plan* plan, const Pipe
     };
     cudaError_t e = cudaSetDevice(dev);
     if (e != cudaSuccess) return bad(CHK_ECUDA, "lane cudaSetDevice", e);
-    cudaStream_t ls, cs;
+    cudaStream_t ls;
     if ((e = cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking)) != cudaSuccess)
       return bad(CHK_ECUDA, "lane stream", e);
-    if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess) {
-      cudaStreamDestroy(ls);
-      return bad(CHK_ECUDA, "lane copy stream", e);
-    }
     char* base = static_cast<char*>(workspace) + (size_t)lane * (slot_bytes + solver_bytes);
     double* d_f = reinterpret_cast<double*>(base);
     double* d_u = d_f + nb * chunk;
@@ -1077,13 +1002,10 @@ int host_pipeline(const chk_grid* grid, const chk_precond_plan* plan, const Pipe
           break;
         }
       }
-      EagerDownload eager;
-      eager.u_host = u_host + nb * b0;
-      eager.cs = cs;
       const int rc = solve_batched_impl(grid, plan, d_b, d_f, d_u, nbc, opts, iterations ? iterations + b0 : nullptr,
                                         final_rel ? final_rel + b0 : nullptr, status ? status + b0 : nullptr,
                                         rhs_projected ? rhs_projected + b0 : nullptr, nullptr, solver_ws,
-                                        solver_bytes, ls, &eager);
+                                        solver_bytes, ls);
       o.launches += g_launches;
       if (rc) {
         o.rc = rc;
@@ -1099,12 +1021,12 @@ int host_pipeline(const chk_grid* grid, const chk_precond_plan* plan, const Pipe
           break;
         }
       }
-      // u came down during the solve (early download) -- the lane's stream already
-      // waits for the last copy
+      if ((e = cudaMemcpyAsync(u_host + nb * b0, d_u, sizeof(double) * nb * nbc, cudaMemcpyDeviceToHost, ls))) {
+        bad(CHK_ECUDA, "download", e);
+        break;
+      }
     }
     if ((e = cudaStreamSynchronize(ls)) != cudaSuccess && o.rc == CHK_OK) bad(CHK_ECUDA, "lane synchronize", e);
-    if ((e = cudaStreamSynchronize(cs)) != cudaSuccess && o.rc == CHK_OK) bad(CHK_ECUDA, "copy synchronize", e);
-    cudaStreamDestroy(cs);
     cudaStreamDestroy(ls);
   };
   if (lanes == 1) {
@@ -1304,7 +1226,7 @@ int32_t chk_slab_phase_planes(const chk_grid* grid, const chk_precond_plan* plan
       case CHK_SLAB_MEANU_APPLY: {
         if ((rc = decide(DECIDE_MEANU))) break;
         const size_t nb = (size_t)sg.nloc * n * n;
-        sub_mean_kernel<<<1184, 256, 0, s>>>(u, w.st, nb, B, 0);
+        sub_mean_kernel<<<1184, 256, 0, s>>>(u, w.st, nb, B);
         CHK_LAUNCHED();
         break;
       }

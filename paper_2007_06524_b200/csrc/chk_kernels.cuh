@@ -60,7 +60,7 @@ struct RState {
   int status;
   int iters;
   int rhs_projected;
-  int done;          // early-download finalisation ran (host pipeline), 0 otherwise
+  int pad0;
   double normf;      // ||f|| after the optional mean projection (solver.py:132,142)
   double norm_pf;    // sqrt|r0.z0| (solver.py:156)
   double mean_f;     // mean removed from f when projected
@@ -2064,7 +2064,6 @@ __global__ void __launch_bounds__(256) mean_u_kernel(const double* __restrict__ 
   const int x0 = rem / G, gg = rem - (rem / G) * G;
   const size_t nb = (size_t)sg.nloc * N * N;
   RState* st = ctl.st + b;
-  if (st->done) return;  // finalised early (its projection already applied)
   double s = 0.0;
   for (int i = threadIdx.x; i < NR * N; i += blockDim.x) {
     const int t = i / N, x2 = i - (i / N) * N;
@@ -2080,18 +2079,14 @@ __global__ void __launch_bounds__(256) mean_u_kernel(const double* __restrict__ 
   }
 }
 
-// mark: the early-download finalisation of one realization (sets RState.done so
-// the batch-wide projection at the end skips it)
-__global__ void __launch_bounds__(256) sub_mean_kernel(double* __restrict__ u, RState* st,
-                                                       size_t nb, int B, int mark) {
+__global__ void __launch_bounds__(256) sub_mean_kernel(double* __restrict__ u, const RState* st,
+                                                       size_t nb, int B) {
   const size_t total = nb * (size_t)B;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const int b = (int)(i / nb);
-    if (!mark && st[b].done) continue;
     u[i] -= st[b].mean_u;  // solver.py:169 (applied once: proj is linear and idempotent)
   }
-  if (mark && blockIdx.x == 0 && threadIdx.x == 0) st[0].done = 1;
 }
 
 // Slab mode: decisions from the allreduced sums red[B][4] (identical on every
