@@ -102,6 +102,41 @@ int fail(int code, const std::string& msg) {
     if (e_ != cudaSuccess) return fail(CHK_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
   } while (0)
 
+// Tensor map of the interleaved spectrum layout (n = 256): the exchange buffer as
+// a 4-D float64 tensor {4 doubles of a 32-byte piece, G groups (stride 32 B),
+// ncols/W pieces (stride G*W*16 B), P*B*nloc rows (stride G*ncols*16 B)}; the
+// plane CTAs store / load boxes {4, 1, TmapBox, 1} (cp.async.bulk.tensor).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+template <int G, int W, int BOX>
+static int plane_tmap(const double2* S, int B, const SlabGeo& sg, CUtensorMap* out) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(CHK_ECUDA, "cuTensorMapEncodeTiled is not available");
+  const cuuint64_t dims[4] = {2 * W, (cuuint64_t)G, (cuuint64_t)(sg.ncols / W), (cuuint64_t)sg.P * B * sg.nloc};
+  const cuuint64_t strides[3] = {(cuuint64_t)W * 16, (cuuint64_t)G * W * 16, (cuuint64_t)G * sg.ncols * 16};
+  const cuuint32_t box[4] = {2 * W, 1, BOX, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double2*>(S), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CHK_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return CHK_OK;
+}
+
 // Tile geometry per grid size: G interleaved x1 groups per plane slab, W
 // spectral columns per middle-pass tile.
 template <int N>
@@ -195,23 +230,38 @@ struct Ops {
     kernel<<<grid, PlaneNT<N>::value, sm, s>>>(args...);
     return cudaSuccess;
   }
+  // the interleaved layout's tensor map; *use = 0 (cp.async path) for the contiguous
+  // layout or a slab chunk that is not a whole number of boxes
+  static int tmap(const double2* S, int B, const SlabGeo& sg, CUtensorMap* tm, int* use) {
+    *tm = CUtensorMap{};
+    *use = 0;
+    if constexpr (IlW<N>::value > 0) {
+      if ((sg.ncols / W) % TmapBox<N>::value) return CHK_OK;
+      *use = 1;
+      return plane_tmap<G, W, TmapBox<N>::value>(S, B, sg, tm);
+    }
+    return CHK_OK;
+  }
   static int fwd(int mode, cudaStream_t s, int B, Geo g, const double* beta, const double* src,
                  double* u, double2* S, PlanDev pl, SolveCtl ctl, int it, SlabGeo sg = whole()) {
     const size_t sm = plane_smem();
     dim3 grid(B * sg.nrun * G);
+    CUtensorMap tm;
+    int use_tm = 0;
+    if (int rc = tmap(S, B, sg, &tm, &use_tm)) return rc;
     ProfScope ps(1, s);
     if (mode == FWD_APPLY) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_APPLY, false>, sm));
-      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_APPLY, false>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it));
+      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_APPLY, false>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it, tm, use_tm));
     } else if (mode == FWD_INIT) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_INIT, false>, sm));
-      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_INIT, false>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it));
+      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_INIT, false>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it, tm, use_tm));
     } else if (allin(g)) {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_Q, true>, sm));
-      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_Q, true>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it));
+      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_Q, true>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it, tm, use_tm));
     } else {
       CHK_CUDA(allow_smem(fwd_plane_kernel<N, G, FWD_Q, false>, sm));
-      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_Q, false>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it));
+      CHK_CUDA(plaunch(fwd_plane_kernel<N, G, FWD_Q, false>, grid, sm, s, g, beta, src, u, S, pl, ctl, sg, B, it, tm, use_tm));
     }
     CHK_LAUNCHED();
     return CHK_OK;
@@ -281,16 +331,19 @@ struct Ops {
                  PlanDev pl, SolveCtl ctl, int it, SlabGeo sg = whole()) {
     const size_t sm = plane_smem();
     dim3 grid(B * sg.nrun * G);
+    CUtensorMap tm;
+    int use_tm = 0;
+    if (int rc = tmap(S, B, sg, &tm, &use_tm)) return rc;
     ProfScope ps(3, s);
     if (mode == INV_APPLY) {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_APPLY>, sm));
-      CHK_CUDA(plaunch(inv_plane_kernel<N, G, INV_APPLY>, grid, sm, s, S, out, u, pl, ctl, sg, B, it));
+      CHK_CUDA(plaunch(inv_plane_kernel<N, G, INV_APPLY>, grid, sm, s, S, out, u, pl, ctl, sg, B, it, tm, use_tm));
     } else if (mode == INV_INIT) {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_INIT>, sm));
-      CHK_CUDA(plaunch(inv_plane_kernel<N, G, INV_INIT>, grid, sm, s, S, out, u, pl, ctl, sg, B, it));
+      CHK_CUDA(plaunch(inv_plane_kernel<N, G, INV_INIT>, grid, sm, s, S, out, u, pl, ctl, sg, B, it, tm, use_tm));
     } else {
       CHK_CUDA(allow_smem(inv_plane_kernel<N, G, INV_ITER>, sm));
-      CHK_CUDA(plaunch(inv_plane_kernel<N, G, INV_ITER>, grid, sm, s, S, out, u, pl, ctl, sg, B, it));
+      CHK_CUDA(plaunch(inv_plane_kernel<N, G, INV_ITER>, grid, sm, s, S, out, u, pl, ctl, sg, B, it, tm, use_tm));
     }
     CHK_LAUNCHED();
     return CHK_OK;

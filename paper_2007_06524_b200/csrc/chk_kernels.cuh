@@ -116,6 +116,13 @@ struct SlabGeo {
 #ifndef CHK_NT512
 #define CHK_NT512 512
 #endif
+// pieces per tensor-map box of the interleaved layout: ncols/W = 2064/P at n = 256,
+// boxes of 172 pieces (5.5 KB, 128-byte aligned in shared memory) for P = 1, 2, 4;
+// P = 8 keeps the cp.async path
+template <int N>
+struct TmapBox {
+  static constexpr int value = 172;
+};
 template <int N>
 struct IlW {
   static constexpr int value = (N == 256) ? 2 : 0;
@@ -883,12 +890,12 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
                                                const double* __restrict__ src,  // x (APPLY) / f (INIT) / p (Q)
                                                double* __restrict__ u, double2* __restrict__ S,
                                                const PlanDev& pl, const SolveCtl& ctl, const SlabGeo& sg,
-                                               int B, int it, int bid) {
+                                               int B, int it, int bid, const CUtensorMap* tmap = nullptr) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
   constexpr int HP = H;
-  extern __shared__ double2 buf[];
+  extern __shared__ __align__(128) double2 buf[];
   __shared__ double scratch[64];
   const int nlg = sg.nloc * G;                        // CTAs per realization (all planes)
   const int b = bid / (sg.nrun * G);
@@ -1010,7 +1017,20 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
     // interleaved layout: 32-byte pieces at a stride of G*W complex
     constexpr int IW = IlW<N>::value;
     static_assert(IW == 2, "pieces are two complex values");
-    {
+    if (tmap) {
+      // tensor-map TMA store: box {4 doubles, 1 group, TPB pieces, 1 row} from the dense
+      // smem row to the 32-byte pieces at a stride of G*W complex (chk_plane_tmap)
+      if (threadIdx.x == 0) {
+        const int npc = sg.ncols / IW;
+        for (int c = 0; c < sg.P; ++c) {
+          const int row = (c * B + b) * sg.nloc + x0l;
+          for (int i0 = 0; i0 < npc; i0 += TmapBox<N>::value)
+            tma_store_4d(tmap, buf + (size_t)c * sg.ncols + (size_t)i0 * IW, 0, gg, i0, row);
+        }
+        bulk_commit();
+        bulk_wait_read0();
+      }
+    } else {
       const int npc = sg.ncols / IW;
       for (int c = 0; c < sg.P; ++c) {
         double* dst = reinterpret_cast<double*>(S + slab_row(sg, B, G, c, b, x0l, 0) + gg * IW);
@@ -1186,7 +1206,7 @@ __device__ __forceinline__ void mid_dtile(double* coef, double* Dsm, const PlanD
 template <int N, int G, int W>
 __global__ void __launch_bounds__(256) dtile_kernel(PlanDev pl, double* __restrict__ Dout) {
   constexpr int GW = G * W;
-  extern __shared__ double dsh[];
+  extern __shared__ __align__(128) double dsh[];
   __shared__ int s_k1[GW], s_k2[GW];
   __shared__ double s_wgt[GW];
   const int r1 = pl.kind == KIND_LKR ? pl.r1 : 0;
@@ -1265,7 +1285,7 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
   const size_t GSTR = IL ? (size_t)W : (size_t)sg.ncols;  // stride between the groups of a column
   const int TILES = sg.tiles;
   const int nsh = __ffs(sg.nloc) - 1;
-  extern __shared__ double2 buf[];
+  extern __shared__ __align__(128) double2 buf[];
   const int doff = mid_dsm_offset(N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
   double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
   __shared__ double scratch[64];
@@ -1412,7 +1432,7 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
                 "x0 radix order 2, 8, 8, 2");
   const int TILES = sg.tiles;
   const int nsh = __ffs(sg.nloc) - 1;
-  extern __shared__ double2 buf[];  // [N][RS]
+  extern __shared__ __align__(128) double2 buf[];  // [N][RS]
   __shared__ double scratch[64];
   __shared__ int s_k1[GW], s_k2[GW];
   __shared__ double s_wgt[GW];
@@ -1602,7 +1622,7 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
   constexpr int ITEMS_B = GW * RA;
   static_assert(NB % P == 0, "NB must be a multiple of P");
   static_assert(RA == Radix<N>::value, "phase A must be the first stage of fft_smem<N> (dig_freq order)");
-  extern __shared__ double2 buf[];  // [P][N][RS] (aliased by the [r1][GW] coefficients)
+  extern __shared__ __align__(128) double2 buf[];  // [P][N][RS] (aliased by the [r1][GW] coefficients)
   const int doff = mid_dsm_offset(P * N * RS, GW, pl.kind == KIND_LKR ? pl.r1 : 0);
   double* Dsm = reinterpret_cast<double*>(reinterpret_cast<char*>(buf) + doff);  // [N][GW]
   __shared__ double scratch[64];
@@ -1906,12 +1926,13 @@ enum : int { INV_APPLY = 0, INV_INIT = 1, INV_ITER = 2 };
 template <int N, int G, int MODE>
 __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, double* __restrict__ out,
                                                double* __restrict__ u, const PlanDev& pl, const SolveCtl& ctl,
-                                               const SlabGeo& sg, int B, int it, int bid) {
+                                               const SlabGeo& sg, int B, int it, int bid,
+                                               const CUtensorMap* tmap = nullptr) {
   constexpr int NR = N / G;
   constexpr int N2 = N / 2;
   constexpr int H = N2 + 1;
   constexpr int HP = H;
-  extern __shared__ double2 buf[];
+  extern __shared__ __align__(128) double2 buf[];
   __shared__ alignas(8) uint64_t bar;
   const int b = bid / (sg.nrun * G);
   const int rrun = bid - b * (sg.nrun * G);
@@ -1932,7 +1953,19 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
   }
   constexpr int IW = IlW<N>::value;
   if constexpr (IW > 0) {
-    if (do_p) {
+    if (do_p && tmap) {
+      // tensor-map TMA load of the 32-byte pieces into the dense smem row
+      if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_arrive_expect_tx(&bar, (uint32_t)(NR * H * sizeof(double2)));
+        const int npc = sg.ncols / IW;
+        for (int c = 0; c < sg.P; ++c) {
+          const int row = (c * B + b) * sg.nloc + x0;
+          for (int i0 = 0; i0 < npc; i0 += TmapBox<N>::value)
+            tma_load_4d(buf + (size_t)c * sg.ncols + (size_t)i0 * IW, tmap, 0, gg, i0, row, &bar);
+        }
+      }
+    } else if (do_p) {
       // interleaved layout: 16-byte cp.async copies of the 32-byte pieces
       for (int c = 0; c < sg.P; ++c) {
         const double2* src = S + slab_row(sg, B, G, c, b, x0, 0) + gg * IW;
@@ -1960,8 +1993,13 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
   }
   if (do_p) {
     if constexpr (IW > 0) {
-      cp_async_wait_all();
-      __syncthreads();
+      if (tmap) {
+        __syncthreads();  // barrier initialised before anyone waits
+        mbar_wait(&bar, 0);
+      } else {
+        cp_async_wait_all();
+        __syncthreads();
+      }
     } else {
       __syncthreads();  // barrier initialised before anyone waits
       mbar_wait(&bar, 0);

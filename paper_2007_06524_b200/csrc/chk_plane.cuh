@@ -18,15 +18,19 @@ template <int N, int G, int MODE, bool ALLIN>
 __global__ void __launch_bounds__(PlaneNT<N>::value, PlaneNT<N>::minb) fwd_plane_kernel(Geo g, const double* __restrict__ beta,
                                                         const double* __restrict__ src, double* __restrict__ u,
                                                         double2* __restrict__ S, PlanDev pl,
-                                                        SolveCtl ctl, SlabGeo sg, int B, int it) {
-  fwd_plane_body<N, G, MODE, ALLIN>(g, beta, src, u, S, pl, ctl, sg, B, it, blockIdx.x);
+                                                        SolveCtl ctl, SlabGeo sg, int B, int it,
+                                                        const __grid_constant__ CUtensorMap tmap, int use_tmap) {
+  fwd_plane_body<N, G, MODE, ALLIN>(g, beta, src, u, S, pl, ctl, sg, B, it, blockIdx.x,
+                                    (IlW<N>::value > 0 && use_tmap) ? &tmap : nullptr);
 }
 
 template <int N, int G, int MODE>
 __global__ void __launch_bounds__(PlaneNT<N>::value, PlaneNT<N>::minb) inv_plane_kernel(const double2* __restrict__ S,
                                                         double* __restrict__ out, double* __restrict__ u,
-                                                        PlanDev pl, SolveCtl ctl, SlabGeo sg, int B, int it) {
-  inv_plane_body<N, G, MODE>(S, out, u, pl, ctl, sg, B, it, blockIdx.x);
+                                                        PlanDev pl, SolveCtl ctl, SlabGeo sg, int B, int it,
+                                                        const __grid_constant__ CUtensorMap tmap, int use_tmap) {
+  inv_plane_body<N, G, MODE>(S, out, u, pl, ctl, sg, B, it, blockIdx.x,
+                             (IlW<N>::value > 0 && use_tmap) ? &tmap : nullptr);
 }
 
 // Paired plane pass: the forward pass of one half of the batch (q = A p, FFT;
