@@ -34,6 +34,12 @@
 #ifndef CHK_FWD_CS  // n = 256 plane passes: CTA-uniform cell-row de-duplication + half-row halo shuffles
 #define CHK_FWD_CS 1
 #endif
+#ifndef CHK_INV_PF_LATE  // n >= CHK_INV_PF_LATE_MIN: the same prefetch just before the last inverse FFT stage
+#define CHK_INV_PF_LATE 1
+#endif
+#ifndef CHK_INV_PF_LATE_MIN
+#define CHK_INV_PF_LATE_MIN 256
+#endif
 #ifndef CHK_INV_PF  // L2 prefetch of the p / u rows at the start of the inverse pass (n <= 128;
 #define CHK_INV_PF 1    // at n >= 256 the prefetched rows are evicted before use: +38 % DRAM reads)
 #endif
@@ -2006,6 +2012,13 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     }
     fft_smem<NR, true, H>(buf, ColAddr{HP}, pl.tw, N);
     c2r_pre<N>(buf, NR, HP, pl.tw);
+    if (MODE == INV_ITER && CHK_INV_PF_LATE && N >= CHK_INV_PF_LATE_MIN && threadIdx.x < NR) {
+      // n >= 256: warm L2 with this slab's p / u rows one stage (not the whole pass)
+      // before they are read -- prefetched at the start they were evicted first
+      const size_t ro = b * nb + ((size_t)x0 * N + gg + G * threadIdx.x) * N;
+      bulk_prefetch_l2(out + ro, N * sizeof(double));
+      if (do_u) bulk_prefetch_l2(u + ro, N * sizeof(double));
+    }
     __syncthreads();
     fft_smem<N2, true, NR>(buf, RowAddr{HP}, pl.tw, N);
   }
