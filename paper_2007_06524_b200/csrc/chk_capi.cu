@@ -20,6 +20,7 @@
 #include "../../include/chk_pcg.h"
 #include "chk_kernels.cuh"
 #include "chk_sample.cuh"
+#include "chk_generic.cuh"
 
 using namespace chk;
 
@@ -433,10 +434,19 @@ int pair_split(int B) {
   return (ctas >= 2LL * 148 && Bb >= Ba) ? Ba : 0;
 }
 
+// fused fast path: the power-of-two sizes of the BASELINE configurations
 bool supported_n(int n) { return n >= 8 && n <= 512 && (n & (n - 1)) == 0; }
+// every other n = n0 * L (n0 a power of two >= 4, so n is a multiple of 4) runs the
+// generic kernels (chk_generic.cuh); the direct Fourier sums stage 16 lines of n
+// complex values in shared memory, which bounds n
+constexpr int GEN_MAX_N = 720;
+constexpr int GEN_TL = 16;
+bool generic_n(int n) { return n >= 4 && n <= GEN_MAX_N && n % 4 == 0 && !supported_n(n); }
+bool any_n(int n) { return supported_n(n) || generic_n(n); }
 
 int maxblk_of(int n) {
   int m = 0;
+  if (generic_n(n)) return n;
   switch (n) {
     case 8: m = Ops<8>::maxblk(); break;
     case 16: m = Ops<16>::maxblk(); break;
@@ -452,7 +462,8 @@ int maxblk_of(int n) {
 int check_grid(const chk_grid* g, Geo* out) {
   if (!g) return fail(CHK_EINVAL, "grid is NULL");
   if (g->d != 3) return fail(CHK_EUNSUPPORTED, "only d = 3 is implemented on the GPU path");
-  if (!supported_n(g->n)) return fail(CHK_EUNSUPPORTED, "n must be a power of two in [8, 512]");
+  if (!any_n(g->n))
+    return fail(CHK_EUNSUPPORTED, "n must be a multiple of 4 in [4, " + std::to_string(GEN_MAX_N) + "] (or a power of two <= 512)");
   if (g->n0 < 4 || (g->n0 & (g->n0 - 1)) || g->L < 1 || g->n0 * g->L != g->n)  // lattice.py:122-123
     return fail(CHK_EINVAL, "need n = n0 * L with n0 a power of two >= 4");
   if (g->k < 1 || g->k > g->n0 || g->offset < 0 || g->offset + g->k > g->n0)
@@ -474,6 +485,10 @@ struct Workspace {
   RState* st;
   double* hist;
   size_t bytes;
+  // generic sizes: residual and q / z in real space, rank-free reduction slots
+  double* r;
+  double* q;
+  double* red;
 };
 
 Workspace carve(void* base, int n, int B, int max_iter) {
@@ -482,6 +497,18 @@ Workspace carve(void* base, int n, int B, int max_iter) {
   char* c = static_cast<char*>(base);
   Workspace w{};
   size_t off = 0;
+  if (generic_n(n)) {
+    w.p = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * nb * B);
+    w.r = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * nb * B);
+    w.q = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * nb * B);
+    w.S = reinterpret_cast<double2*>(c + off); off = align_up(off + sizeof(double2) * nb * B);
+    w.part = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * 2 * (size_t)n * B);
+    w.red = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * 4 * (size_t)B);
+    w.st = reinterpret_cast<RState*>(c + off); off = align_up(off + sizeof(RState) * B);
+    w.hist = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * (size_t)max_iter * B);
+    w.bytes = off;
+    return w;
+  }
   w.p = reinterpret_cast<double*>(c + off); off = align_up(off + sizeof(double) * nb * B);
   w.Rh = reinterpret_cast<double2*>(c + off); off = align_up(off + sizeof(double2) * spec * B);
   w.S = reinterpret_cast<double2*>(c + off); off = align_up(off + sizeof(double2) * spec * B);
@@ -513,6 +540,136 @@ struct PinnedStates {
   }
 };
 thread_local PinnedStates g_pinned;
+
+// ---- generic grid sizes (chk_generic.cuh) ----
+// z = P x for the B complex arrays already in S (x + 0 i): forward sums along x2,
+// x1, x0, scaling by D / n^3, inverse sums along x0, x1, x2 (the last one leaves
+// the real part in z).  st != null: only active realizations.
+int gen_precond(cudaStream_t s, int B, int n, double2* S, const PlanDev& pl, int project, const RState* st,
+                double* z) {
+  const size_t sm = sizeof(double2) * ((size_t)n * GEN_TL + n);
+  CHK_CUDA(Ops<8>::allow_smem(gen_dft_axis_kernel<false>, sm));
+  CHK_CUDA(Ops<8>::allow_smem(gen_dft_axis_kernel<true>, sm));
+  const dim3 grid((n * n + GEN_TL - 1) / GEN_TL, B);
+  for (int axis = 2; axis >= 0; --axis) {
+    gen_dft_axis_kernel<false><<<grid, 256, sm, s>>>(S, pl.tw, n, axis, GEN_TL, st, nullptr);
+    CHK_LAUNCHED();
+  }
+  gen_scale_kernel<<<dim3(n, B), 256, 0, s>>>(S, pl, n, project, st);
+  CHK_LAUNCHED();
+  for (int axis = 0; axis <= 2; ++axis) {
+    gen_dft_axis_kernel<true><<<grid, 256, sm, s>>>(S, pl.tw, n, axis, GEN_TL, st, axis == 2 ? z : nullptr);
+    CHK_LAUNCHED();
+  }
+  return CHK_OK;
+}
+
+// Batched PCG (solver.py:118-194) for a generic grid size; same per-realization
+// state, decisions (decide_kernel) and reporting as the fused path.
+int gen_solve(const Geo& g, const PlanDev& pl, const double* beta, const double* f, double* u, int B,
+              const chk_pcg_opts* opts, int32_t* iterations, double* final_rel, int32_t* status,
+              int32_t* rhs_projected, double* history, const Workspace& w, cudaStream_t s) {
+  const int n = g.n;
+  const double ntot = (double)n * n * n;
+  const dim3 grid(n, B);
+  SolveCtl ctl{w.st, nullptr, w.part, w.hist, n, opts->max_iter, opts->tol, opts->precond_residual_stopping ? 1 : 0,
+               w.red, 0};
+  RState* hst_all = g_pinned.get((size_t)2 * B);
+  if (!hst_all) return fail(CHK_ECUDA, "cudaMallocHost failed");
+  CHK_CUDA(cudaMemsetAsync(w.st, 0, sizeof(RState) * B, s));
+  CHK_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(double) * (size_t)opts->max_iter * B, s));
+  CHK_CUDA(cudaMemsetAsync(w.red, 0, sizeof(double) * 4 * B, s));
+  cudaEvent_t ev[2];
+  CHK_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CHK_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  auto finalize = [&](int slot0, int slot1) -> int {
+    gen_finalize_kernel<<<B, 256, 0, s>>>(w.part, n, slot0 >= 0 ? w.red + slot0 : nullptr,
+                                          slot1 >= 0 ? w.red + slot1 : nullptr, 4);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  };
+  auto decide = [&](int what, int it) -> int {
+    decide_kernel<<<1, 256, 0, s>>>(ctl, w.red, B, what, it, ntot);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  };
+  // z = P r (mean-projected) into w.q, then ||r||^2 and r.z, decisions, direction update
+  auto precond_step = [&](int it) -> int {
+    int rc2;
+    gen_residual_kernel<<<grid, 256, 0, s>>>(w.r, w.q, w.S, n, w.st, it);
+    CHK_LAUNCHED();
+    if ((rc2 = gen_precond(s, B, n, w.S, pl, 1, w.st, w.q))) return rc2;
+    gen_dots_kernel<<<grid, 256, 0, s>>>(w.r, w.q, n, w.part, w.st);
+    CHK_LAUNCHED();
+    if ((rc2 = finalize(1, 2))) return rc2;
+    if ((rc2 = decide(DECIDE_MID, it))) return rc2;
+    gen_update_kernel<<<grid, 256, 0, s>>>(w.p, u, w.q, n, w.st, it);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  };
+  auto run = [&]() -> int {
+    int rc2;
+    // r = f (projected), u = 0, z = P r, p = z  (solver.py:131-156)
+    gen_stats_kernel<<<grid, 256, 0, s>>>(f, n, w.part);
+    CHK_LAUNCHED();
+    if ((rc2 = finalize(0, 1))) return rc2;
+    if ((rc2 = decide(DECIDE_STATS, 0))) return rc2;
+    gen_init_kernel<<<grid, 256, 0, s>>>(f, w.r, u, n, w.st);
+    CHK_LAUNCHED();
+    if ((rc2 = precond_step(0))) return rc2;
+    const int chunk = 4;
+    bool pending = false;
+    int ev_i = 0;
+    for (int it = 1; it <= opts->max_iter; ++it) {
+      // q = A p, p.q -> alpha (solver.py:162-166)
+      gen_stencil_kernel<<<grid, 256, 0, s>>>(g, beta, w.p, w.q, w.part, w.st);
+      CHK_LAUNCHED();
+      if ((rc2 = finalize(0, -1))) return rc2;
+      if ((rc2 = decide(DECIDE_ALPHA, it))) return rc2;
+      // r -= alpha q, stop test, z = P r, beta, u += alpha p, p = z + beta p (solver.py:167-184)
+      if ((rc2 = precond_step(it))) return rc2;
+      if (it % chunk == 0 || it == opts->max_iter) {
+        if (pending) {
+          CHK_CUDA(cudaEventSynchronize(ev[ev_i ^ 1]));
+          const RState* prev = hst_all + (size_t)(ev_i ^ 1) * B;
+          bool any = false;
+          for (int b = 0; b < B; ++b) any |= (prev[b].status == ST_ACTIVE);
+          if (!any) break;
+        }
+        CHK_CUDA(cudaMemcpyAsync(hst_all + (size_t)ev_i * B, w.st, sizeof(RState) * B, cudaMemcpyDeviceToHost, s));
+        CHK_CUDA(cudaEventRecord(ev[ev_i], s));
+        ev_i ^= 1;
+        pending = true;
+      }
+    }
+    // final projection of u (solver.py:169; applied once)
+    gen_sum_kernel<<<grid, 256, 0, s>>>(u, n, w.part);
+    CHK_LAUNCHED();
+    if ((rc2 = finalize(3, -1))) return rc2;
+    if ((rc2 = decide(DECIDE_MEANU, 0))) return rc2;
+    sub_mean_kernel<<<1184, 256, 0, s>>>(u, w.st, (size_t)n * n * n, B);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  };
+  const int rc = run();
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  if (rc) return rc;
+  RState* hst = hst_all;
+  CHK_CUDA(cudaMemcpyAsync(hst, w.st, sizeof(RState) * B, cudaMemcpyDeviceToHost, s));
+  if (history)
+    CHK_CUDA(cudaMemcpyAsync(history, w.hist, sizeof(double) * (size_t)opts->max_iter * B, cudaMemcpyDeviceToHost, s));
+  CHK_CUDA(cudaStreamSynchronize(s));
+  for (int b = 0; b < B; ++b) {
+    int stt = hst[b].status;
+    if (stt == ST_ACTIVE) stt = ST_NOT_CONVERGED;
+    if (status) status[b] = stt;
+    if (iterations) iterations[b] = hst[b].iters;
+    if (final_rel) final_rel[b] = hst[b].final_rel;
+    if (rhs_projected) rhs_projected[b] = hst[b].rhs_projected;
+  }
+  return CHK_OK;
+}
 
 }  // namespace
 
@@ -594,7 +751,7 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
                                 const double* eigenvalues, double delta, chk_precond_plan** out) {
   if (!out) return fail(CHK_EINVAL, "out is NULL");
   *out = nullptr;
-  if (!supported_n(n)) return fail(CHK_EUNSUPPORTED, "n must be a power of two in [8, 512]");
+  if (!any_n(n)) return fail(CHK_EUNSUPPORTED, "unsupported grid size n = " + std::to_string(n));
   if (kind != CHK_PRECOND_LKR && kind != CHK_PRECOND_FOURIER && kind != CHK_PRECOND_REGULARIZED)
     return fail(CHK_EINVAL, "unknown preconditioner kind");
   if (kind == CHK_PRECOND_LKR && (factors == nullptr || r1 < 1 || r1 > 512))
@@ -619,12 +776,25 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
     tw[3 * n / 4] = make_double2(0.0, 1.0);
   }
   cudaError_t e;
+  {
+    // constant-memory twiddles of the plane passes (c_tw512; per device, same values every time)
+    std::vector<double2> t5(512);
+    for (int k = 0; k < 512; ++k) {
+      long double a = 2.0L * 3.14159265358979323846264338327950288L * (long double)k / 512.0L;
+      t5[k] = make_double2((double)cosl(a), (double)(-sinl(a)));
+    }
+    t5[0] = make_double2(1.0, 0.0);
+    t5[128] = make_double2(0.0, -1.0);
+    t5[256] = make_double2(-1.0, 0.0);
+    t5[384] = make_double2(0.0, 1.0);
+    if ((e = cudaMemcpyToSymbol(c_tw512, t5.data(), sizeof(double2) * 512)) != cudaSuccess) goto cuda_fail;
+  }
   if ((e = cudaMalloc(&p->d_tw, sizeof(double2) * n)) != cudaSuccess) goto cuda_fail;
   if ((e = cudaMemcpy(p->d_tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice)) != cudaSuccess) goto cuda_fail;
   if (kind == CHK_PRECOND_LKR) {
     if ((e = cudaMalloc(&p->d_U, sizeof(double) * 3 * (size_t)r1 * n)) != cudaSuccess) goto cuda_fail;
     if ((e = cudaMemcpy(p->d_U, factors, sizeof(double) * 3 * (size_t)r1 * n, cudaMemcpyHostToDevice)) != cudaSuccess) goto cuda_fail;
-    {
+    if (supported_n(n)) {
       std::vector<double> up((size_t)r1 * n);
       for (int r = 0; r < r1; ++r)
         for (int q = 0; q < n; ++q) up[(size_t)r * n + q] = factors[(size_t)r * n + host_dig_freq(n, q)];
@@ -638,7 +808,7 @@ int32_t chk_precond_plan_create(int32_t kind, int32_t n, int32_t r1, const doubl
   // diagonal tiles of every middle-pass tile (n^2 (n/2+1) doubles: 8.5 MB at
   // n = 128, 539 MB at n = 512); CHK_NO_DTILE=1 evaluates them per CTA instead
   // (n = 256 always has the table: its middle pass reads it)
-  if (!(getenv("CHK_NO_DTILE") && atoi(getenv("CHK_NO_DTILE"))) || (n == 256 && CHK_R256)) {
+  if (supported_n(n) && (!(getenv("CHK_NO_DTILE") && atoi(getenv("CHK_NO_DTILE"))) || (n == 256 && CHK_R256))) {
     const int rc2 = plan_dtiles(p);
     if (rc2) {
       chk_precond_plan_destroy(p);
@@ -666,6 +836,7 @@ int32_t chk_precond_plan_destroy(chk_precond_plan* p) {
 size_t chk_precond_workspace_bytes(const chk_precond_plan* p, int32_t B) {
   if (!p || B < 1) return 0;
   const size_t n = p->n;
+  if (generic_n(p->n)) return align_up(sizeof(double2) * n * n * n * (size_t)B);
   return align_up(sizeof(double2) * n * n * (n / 2 + 1) * (size_t)B);
 }
 
@@ -681,6 +852,11 @@ int32_t chk_precond_apply(const chk_precond_plan* p, const double* r, double* z,
   Geo g{};
   g.n = p->n;
   int rc = CHK_OK;
+  if (generic_n(p->n)) {
+    gen_load_kernel<<<dim3(p->n, B), 256, 0, s>>>(r, S, p->n);
+    CHK_LAUNCHED();
+    return gen_precond(s, B, p->n, S, pl, 0, nullptr, z);
+  }
   CHK_DISPATCH(p->n, {
     rc = O::fwd(FWD_APPLY, s, B, g, nullptr, r, nullptr, S, pl, ctl, 0);
     if (rc) return rc;
@@ -743,6 +919,15 @@ int32_t chk_stencil_apply(const chk_grid* grid, const double* beta, const double
     cnt = reinterpret_cast<unsigned*>(static_cast<char*>(sc->p) + pb);
     CHK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * B, s));
   }
+  if (generic_n(grid->n)) {
+    gen_stencil_kernel<<<dim3(grid->n, B), 256, 0, s>>>(g, beta, x, y, xy ? part : nullptr, nullptr);
+    CHK_LAUNCHED();
+    if (xy) {
+      gen_finalize_kernel<<<B, 256, 0, s>>>(part, grid->n, xy, nullptr, 1);
+      CHK_LAUNCHED();
+    }
+    return CHK_OK;
+  }
   CHK_DISPATCH(grid->n, { rc = O::stencil(s, B, g, beta, x, y, xy, part, cnt); });
   return rc;
 }
@@ -755,13 +940,18 @@ int32_t chk_corrector_rhs(const chk_grid* grid, const double* beta, double* f, i
   if (!beta || !f || B < 1) return fail(CHK_EINVAL, "bad arguments");
   if (direction < 1 || direction > 3) return fail(CHK_EINVAL, "direction must be in 1..3");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (generic_n(grid->n)) {
+    gen_corrector_rhs_kernel<<<dim3(grid->n, B), 256, 0, s>>>(g, beta, f, direction - 1, scale);
+    CHK_LAUNCHED();
+    return CHK_OK;
+  }
   CHK_DISPATCH(grid->n, { rc = O::rhs(s, B, g, beta, f, direction - 1, scale); });
   return rc;
 }
 
 size_t chk_pcg_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, int32_t B,
                                int32_t max_iter) {
-  if (!grid || !plan || B < 1 || max_iter < 1 || !supported_n(grid->n)) return 0;
+  if (!grid || !plan || B < 1 || max_iter < 1 || !any_n(grid->n)) return 0;
   return carve(nullptr, grid->n, B, max_iter).bytes;
 }
 
@@ -786,6 +976,8 @@ int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const
   if (!workspace || workspace_bytes < w.bytes) return fail(CHK_EINVAL, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   PlanDev pl = plan_dev(plan);
+  if (generic_n(n))
+    return gen_solve(g, pl, beta, f, u, B, opts, iterations, final_rel, status, rhs_projected, history, w, s);
   SolveCtl ctl{w.st, w.Rh, w.part, w.hist, maxblk_of(n), opts->max_iter, opts->tol,
                opts->precond_residual_stopping ? 1 : 0, nullptr, 0};
   RState* hst_all = g_pinned.get((size_t)2 * B);
@@ -943,7 +1135,7 @@ static int host_lanes(int nchunks) {
 
 size_t chk_pcg_host_workspace_bytes(const chk_grid* grid, const chk_precond_plan* plan, int32_t chunk,
                                     int32_t max_iter) {
-  if (!grid || !plan || chunk < 1 || max_iter < 1 || !supported_n(grid->n)) return 0;
+  if (!grid || !plan || chunk < 1 || max_iter < 1 || !any_n(grid->n)) return 0;
   const size_t nb = (size_t)grid->n * grid->n * grid->n;
   const size_t lb = (size_t)grid->L * grid->L * grid->L;
   const size_t slot = align_up(sizeof(double) * (2 * nb + lb) * chunk) + align_up(2 * sizeof(uint64_t) * chunk);
@@ -1047,7 +1239,12 @@ int host_pipeline(const chk_grid* grid, const chk_precond_plan* plan, const Pipe
       } else {
         // PCG load h^(d-1) * h^(2-d) * 1/2 (c[x+e_i] - c[x-e_i])  (homogenize.py:85-89,110)
         int rc = CHK_OK;
-        CHK_DISPATCH_V(grid->n, rc, { rc = O::rhs(ls, nbc, geo, d_b, d_f, in.rhs_dir - 1, h * h * (1.0 / h)); });
+        if (generic_n(grid->n)) {
+          gen_corrector_rhs_kernel<<<dim3(grid->n, nbc), 256, 0, ls>>>(geo, d_b, d_f, in.rhs_dir - 1, h * h * (1.0 / h));
+          if (cudaGetLastError() != cudaSuccess) rc = fail(CHK_ECUDA, "corrector_rhs launch");
+        } else {
+          CHK_DISPATCH_V(grid->n, rc, { rc = O::rhs(ls, nbc, geo, d_b, d_f, in.rhs_dir - 1, h * h * (1.0 / h)); });
+        }
         ++o.launches;
         if (rc) {
           o.rc = rc;
@@ -1225,6 +1422,7 @@ int32_t chk_slab_phase_planes(const chk_grid* grid, const chk_precond_plan* plan
   int rc = check_grid(grid, &g);
   if (rc) return rc;
   if (!plan || plan->n != grid->n || !opts || B < 1 || !red) return fail(CHK_EINVAL, "bad arguments");
+  if (!supported_n(grid->n)) return fail(CHK_EUNSUPPORTED, "slab decomposition needs a power-of-two n in [8, 512]");
   SlabGeo sg;
   if ((rc = slab_geo(grid, slab, halo_lo, halo_hi, &sg))) return rc;
   if (plane_count < 0) plane_count = sg.nloc - plane_begin;

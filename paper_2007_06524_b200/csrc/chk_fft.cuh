@@ -29,6 +29,18 @@ __device__ __forceinline__ double2 cmul_mi(double2 a) {
   return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
 
+// Twiddle sources.  A plan's table w[k] = exp(-2 pi i k / n) lives in global memory
+// (read-only path); for the plane passes, whose shared-memory stages saturate the
+// LSU data pipe, the same values come from constant memory instead (c_tw512, the
+// n = 512 table: every power-of-two table is a stride of it, bit for bit), which
+// takes the warp-uniform twiddle loads off the LSU.
+__constant__ double2 c_tw512[512];
+struct CTw {
+  int mul;  // 512 / (length of the table being emulated)
+};
+__device__ __forceinline__ double2 tw_at(const double2* tw, int i) { return __ldg(tw + i); }
+__device__ __forceinline__ double2 tw_at(CTw t, int i) { return c_tw512[i * t.mul]; }
+
 template <bool INV>
 __device__ __forceinline__ void dft2(double2& a, double2& b) {
   double2 t = a;
@@ -89,9 +101,8 @@ struct Radix {
 // One in-place stage at sub-length M of a length-N transform over `npencil`
 // pencils; element e of pencil p is at buf[addr(p, e)].  Consecutive threads
 // take consecutive pencils (callers lay pencils out bank-conflict free).
-template <int N, int M, bool INV, int NP, class Addr>
-__device__ __forceinline__ void fft_stage(double2* buf, const Addr& addr,
-                                          const double2* __restrict__ tw, int twstride) {
+template <int N, int M, bool INV, int NP, class Addr, class TW>
+__device__ __forceinline__ void fft_stage(double2* buf, const Addr& addr, TW tw, int twstride) {
   constexpr int R = Radix<M>::value;
   constexpr int S = M / R;
   constexpr int NBF = N / R;
@@ -108,12 +119,12 @@ __device__ __forceinline__ void fft_stage(double2* buf, const Addr& addr,
       dftR<R, false>(v);
       if (S > 1) {
 #pragma unroll
-        for (int m = 1; m < R; ++m) v[m] = cmul(v[m], __ldg(tw + (j * m * (N / M)) * twstride));
+        for (int m = 1; m < R; ++m) v[m] = cmul(v[m], tw_at(tw, (j * m * (N / M)) * twstride));
       }
     } else {
       if (S > 1) {
 #pragma unroll
-        for (int m = 1; m < R; ++m) v[m] = cmulc(v[m], __ldg(tw + (j * m * (N / M)) * twstride));
+        for (int m = 1; m < R; ++m) v[m] = cmulc(v[m], tw_at(tw, (j * m * (N / M)) * twstride));
       }
       dftR<R, true>(v);
     }
@@ -124,9 +135,8 @@ __device__ __forceinline__ void fft_stage(double2* buf, const Addr& addr,
 
 template <int N, int M, bool INV, int NP>
 struct FftRec {
-  template <class Addr>
-  __device__ __forceinline__ static void run(double2* buf, const Addr& addr,
-                                             const double2* __restrict__ tw, int twstride) {
+  template <class Addr, class TW>
+  __device__ __forceinline__ static void run(double2* buf, const Addr& addr, TW tw, int twstride) {
     constexpr int R = Radix<M>::value;
     if constexpr (!INV) {
       fft_stage<N, M, false, NP>(buf, addr, tw, twstride);
@@ -144,9 +154,8 @@ struct FftRec {
 // groups of R, no twiddles), so a caller can fuse it with pointwise work.
 template <int N, int M, bool INV, int NP>
 struct FftRecButLast {
-  template <class Addr>
-  __device__ __forceinline__ static void run(double2* buf, const Addr& addr,
-                                             const double2* __restrict__ tw, int twstride) {
+  template <class Addr, class TW>
+  __device__ __forceinline__ static void run(double2* buf, const Addr& addr, TW tw, int twstride) {
     constexpr int R = Radix<M>::value;
     if constexpr (M / R > 1) {
       if constexpr (!INV) {
@@ -176,9 +185,8 @@ struct LastRadix<1> {
 // Full length-N transform; the caller must __syncthreads() before (data in
 // smem); returns after a __syncthreads().  Forward: natural -> digit-reversed.
 // Inverse (unnormalised): digit-reversed -> natural, result scaled by N.
-template <int N, bool INV, int NP, class Addr>
-__device__ __forceinline__ void fft_smem(double2* buf, const Addr& addr,
-                                         const double2* __restrict__ tw, int ntab) {
+template <int N, bool INV, int NP, class Addr, class TW>
+__device__ __forceinline__ void fft_smem(double2* buf, const Addr& addr, TW tw, int ntab) {
   if constexpr (N > 1) FftRec<N, N, INV, NP>::run(buf, addr, tw, ntab / N);
 }
 
@@ -186,7 +194,8 @@ __device__ __forceinline__ void fft_smem(double2* buf, const Addr& addr,
 // index semantics to fft_smem<L> (digit-reversed output), all loops unrolled.
 template <int L, int M, bool INV>
 struct RegFft {
-  __device__ __forceinline__ static void run(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
+  template <class TW>
+  __device__ __forceinline__ static void run(double2 (&v)[L], TW tw, int ntab) {
     constexpr int R = Radix<M>::value, S = M / R;
     if constexpr (INV && S > 1) RegFft<L, S, true>::run(v, tw, ntab);
 #pragma unroll
@@ -200,12 +209,12 @@ struct RegFft {
           dftR<R, false>(a);
           if (j > 0) {
 #pragma unroll
-            for (int m = 1; m < R; ++m) a[m] = cmul(a[m], __ldg(tw + (j * m) * (ntab / M)));
+            for (int m = 1; m < R; ++m) a[m] = cmul(a[m], tw_at(tw, (j * m) * (ntab / M)));
           }
         } else {
           if (j > 0) {
 #pragma unroll
-            for (int m = 1; m < R; ++m) a[m] = cmulc(a[m], __ldg(tw + (j * m) * (ntab / M)));
+            for (int m = 1; m < R; ++m) a[m] = cmulc(a[m], tw_at(tw, (j * m) * (ntab / M)));
           }
           dftR<R, true>(a);
         }
@@ -216,8 +225,8 @@ struct RegFft {
     if constexpr (!INV && S > 1) RegFft<L, S, false>::run(v, tw, ntab);
   }
 };
-template <int L, bool INV>
-__device__ __forceinline__ void reg_fft(double2 (&v)[L], const double2* __restrict__ tw, int ntab) {
+template <int L, bool INV, class TW>
+__device__ __forceinline__ void reg_fft(double2 (&v)[L], TW tw, int ntab) {
   if constexpr (L > 1) RegFft<L, L, INV>::run(v, tw, ntab);
 }
 
@@ -234,8 +243,8 @@ struct LastTwo<1> {
 };
 template <int N, int M, bool INV, int NP, int BL>
 struct FftStop {
-  template <class Addr>
-  __device__ __forceinline__ static void run(double2* buf, const Addr& addr, const double2* __restrict__ tw, int twstride) {
+  template <class Addr, class TW>
+  __device__ __forceinline__ static void run(double2* buf, const Addr& addr, TW tw, int twstride) {
     if constexpr (M > BL) {
       constexpr int R = Radix<M>::value;
       if constexpr (!INV) {

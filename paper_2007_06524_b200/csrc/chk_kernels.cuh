@@ -821,9 +821,8 @@ struct GAddr {  // middle tile: pencil = (x0, w), element = group slot g
 
 // Half-length real FFT post-processing, in place at digit-reversed positions of
 // each row (length N/2 complex + slot N/2 for the Nyquist term).
-template <int N>
-__device__ __forceinline__ void r2c_post(double2* buf, int nrows, int hp,
-                                         const double2* __restrict__ tw) {
+template <int N, class TW>
+__device__ __forceinline__ void r2c_post(double2* buf, int nrows, int hp, TW tw) {
   constexpr int N2 = N / 2;
   constexpr int NP = N2 / 2 + 1;
   for (int i = threadIdx.x; i < nrows * NP; i += blockDim.x) {
@@ -840,8 +839,8 @@ __device__ __forceinline__ void r2c_post(double2* buf, int nrows, int hp,
       row[q] = make_double2(E.x + O.x, 0.0);
       row[N2] = make_double2(E.x - O.x, 0.0);
     } else {
-      const double2 a = cadd(E, cmul(__ldg(tw + k), O));
-      const double2 c = cadd(cconj(E), cmul(__ldg(tw + (N2 - k)), cconj(O)));
+      const double2 a = cadd(E, cmul(tw_at(tw, k), O));
+      const double2 c = cadd(cconj(E), cmul(tw_at(tw, N2 - k), cconj(O)));
       row[q] = a;
       row[qc] = c;
     }
@@ -849,9 +848,8 @@ __device__ __forceinline__ void r2c_post(double2* buf, int nrows, int hp,
 }
 
 // Inverse of r2c_post: X (permuted + Nyquist slot) -> Z at digit-reversed positions.
-template <int N>
-__device__ __forceinline__ void c2r_pre(double2* buf, int nrows, int hp,
-                                        const double2* __restrict__ tw) {
+template <int N, class TW>
+__device__ __forceinline__ void c2r_pre(double2* buf, int nrows, int hp, TW tw) {
   constexpr int N2 = N / 2;
   constexpr int NP = N2 / 2 + 1;
   for (int i = threadIdx.x; i < nrows * NP; i += blockDim.x) {
@@ -863,17 +861,56 @@ __device__ __forceinline__ void c2r_pre(double2* buf, int nrows, int hp,
     const double2 xc = (k == 0) ? row[N2] : row[qc];
     {
       const double2 s = cadd(xk, cconj(xc));
-      const double2 d = cmulc(csub(xk, cconj(xc)), __ldg(tw + k));
+      const double2 d = cmulc(csub(xk, cconj(xc)), tw_at(tw, k));
       // Z = E + i O with E = s/2, O = d/2
       row[q] = make_double2(0.5 * (s.x - d.y), 0.5 * (s.y + d.x));
     }
     if (k != 0 && kc != k) {
       const double2 s = cadd(xc, cconj(xk));
-      const double2 d = cmulc(csub(xc, cconj(xk)), __ldg(tw + kc));
+      const double2 d = cmulc(csub(xc, cconj(xk)), tw_at(tw, kc));
       row[qc] = make_double2(0.5 * (s.x - d.y), 0.5 * (s.y + d.x));
     }
   }
 }
+
+// Twiddle source of the plane passes: constant memory (CHK_CTW, default) or the
+// plan's global table.
+#ifndef CHK_CTW
+#define CHK_CTW 1
+#endif
+// Measured (same box A/B): pair pass n = 128 -3.5 %, fwd / inv n = 256 -3.8 % / -3.6 %;
+// n = 512 (one CTA per SM, latency-bound, not LSU-bound) +1.4 %, so it keeps the table.
+template <int N, bool C>
+struct TwSel {
+  using type = const double2*;
+  __device__ __forceinline__ static type get(const PlanDev& pl) { return pl.tw; }
+};
+template <int N>
+struct TwSel<N, true> {
+  using type = CTw;
+  __device__ __forceinline__ static type get(const PlanDev&) { return CTw{512 / N}; }
+};
+template <int N>
+using PlaneTw = typename TwSel<N, (CHK_CTW != 0 && N <= 256)>::type;
+template <int N>
+__device__ __forceinline__ PlaneTw<N> plane_tw(const PlanDev& pl) { return TwSel<N, (CHK_CTW != 0 && N <= 256)>::get(pl); }
+// middle passes: register FFTs (reg_fft) index the table with compile-time constants,
+// which become constant-bank operands of the multiplies (no load instruction at all):
+// reg_tw.  Stages whose twiddle index varies inside a warp keep the global table
+// (divergent constant loads replay: n = 128 middle pass +30 %, n = 512 +12 % when tried),
+// except in the n = 256 register-phase kernel, where every twiddle from constant memory
+// measured -6 % (mid_tw).
+#ifndef CHK_CTW_MID
+#define CHK_CTW_MID 1
+#endif
+template <int N>
+using RegTw = typename TwSel<N, (CHK_CTW_MID != 0)>::type;
+template <int N>
+__device__ __forceinline__ RegTw<N> reg_tw(const PlanDev& pl) { return TwSel<N, (CHK_CTW_MID != 0)>::get(pl); }
+template <int N>
+using MidTw = typename TwSel<N, (CHK_CTW_MID != 0 && N == 256)>::type;
+template <int N>
+__device__ __forceinline__ MidTw<N> mid_tw(const PlanDev& pl) { return TwSel<N, (CHK_CTW_MID != 0 && N == 256)>::get(pl); }
 
 // ----------------------------------------------------------------------------
 // kernel 1: stencil + forward plane transform
@@ -1010,11 +1047,12 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   }
   __syncthreads();
   // R2C along x2: rows of N reals viewed as N/2 complex (z_m = x_2m + i x_2m+1)
-  fft_smem<N2, false, NR>(buf, RowAddr{HP}, pl.tw, N);
-  r2c_post<N>(buf, NR, HP, pl.tw);
+  const PlaneTw<N> ptw = plane_tw<N>(pl);
+  fft_smem<N2, false, NR>(buf, RowAddr{HP}, ptw, N);
+  r2c_post<N>(buf, NR, HP, ptw);
   __syncthreads();
   // C2C along the x1 group (length NR)
-  fft_smem<NR, false, H>(buf, ColAddr{HP}, pl.tw, N);
+  fft_smem<NR, false, H>(buf, ColAddr{HP}, ptw, N);
   // the slab row is contiguous in smem (HP == H); it leaves in P column chunks
   // (one bulk store each; a single chunk when the grid is not slab-decomposed)
   fence_proxy_async_smem();
@@ -1354,12 +1392,12 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
       for (int g = 0; g < G; ++g) v[g] = S[rbase + (size_t)g * GSTR];
 #pragma unroll
       for (int g = 1; g < G; ++g) v[g] = cmul(v[g], s_tw[g * W + w]);
-      reg_fft<G, false>(v, pl.tw, N);
+      reg_fft<G, false>(v, reg_tw<N>(pl), N);
 #pragma unroll
       for (int g = 0; g < G; ++g) buf[x0 * RS + g * W + w] = v[g];
     }
     __syncthreads();
-    FftRecButLast<N, N, false, GW>::run(buf, X0Addr{RS}, pl.tw, 1);
+    FftRecButLast<N, N, false, GW>::run(buf, X0Addr{RS}, mid_tw<N>(pl), 1);
     // ---- last stage + residual / scaling + first inverse stage (registers) ----
     double rr = 0.0, rz = 0.0;
     double2* Rt = ctl.Rh + ((size_t)b * TILES + tile) * N * GW;
@@ -1386,7 +1424,7 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
       for (int e = 0; e < RL; ++e) buf[(blk * RL + e) * RS + s] = v[e];
     }
     __syncthreads();
-    FftRecButLast<N, N, true, GW>::run(buf, X0Addr{RS}, pl.tw, 1);
+    FftRecButLast<N, N, true, GW>::run(buf, X0Addr{RS}, mid_tw<N>(pl), 1);
     // ---- inverse group combine + store (registers) ----
     for (int item = threadIdx.x; item < N * W; item += blockDim.x) {
       const int w = item % W, x0 = item / W;
@@ -1394,7 +1432,7 @@ __global__ void __launch_bounds__(MidNT<N>::value, DG ? MidNT<N>::minb_dg : MidN
       double2 v[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) v[g] = buf[x0 * RS + g * W + w];
-      reg_fft<G, true>(v, pl.tw, N);
+      reg_fft<G, true>(v, reg_tw<N>(pl), N);
 #pragma unroll
       for (int g = 1; g < G; ++g) v[g] = cmulc(v[g], s_tw[g * W + w]);
 #pragma unroll
@@ -1494,9 +1532,9 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
         for (int g = 1; g < G; ++g) v[h][g] = cmul(v[h][g], s_tw[g * W + wA]);
-        reg_fft<G, false>(v[h], pl.tw, N);
+        reg_fft<G, false>(v[h], reg_tw<N>(pl), N);
       }
-      const double2 t1 = __ldg(pl.tw + jA);
+      const double2 t1 = tw_at(mid_tw<N>(pl), jA);
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const double2 a = cadd(v[0][g], v[1][g]);
@@ -1516,7 +1554,7 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
       dftR<8, false>(v);
       if (jj > 0) {
 #pragma unroll
-        for (int m = 1; m < 8; ++m) v[m] = cmul(v[m], __ldg(pl.tw + jj * m * 2));
+        for (int m = 1; m < 8; ++m) v[m] = cmul(v[m], tw_at(mid_tw<N>(pl), jj * m * 2));
       }
 #pragma unroll
       for (int t = 0; t < 8; ++t) base[16 * t * RS] = v[t];
@@ -1530,7 +1568,7 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
       double2 v[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = row[e * RS];
-      reg_fft<16, false>(v, pl.tw, N);
+      reg_fft<16, false>(v, reg_tw<N>(pl), N);
       double2* Rt = ctl.Rh + ((size_t)b * TILES + tile) * N * GW + (blk * 16) * GW + s;
       const double wgt = s_wgt[s];
       const double al = s_alpha[j];
@@ -1541,7 +1579,7 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
         const double D = (pos0 == 0 && s == s_dc) ? 0.0 : __ldg(Dg + pos0 * GW + s);
         v[e] = mid_point<MODE>(v[e], D, wgt, scale, al, Rt + e * GW, rr, rz);
       }
-      reg_fft<16, true>(v, pl.tw, N);
+      reg_fft<16, true>(v, reg_tw<N>(pl), N);
 #pragma unroll
       for (int e = 0; e < 16; ++e) row[e * RS] = v[e];
     }
@@ -1555,7 +1593,7 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
       for (int t = 0; t < 8; ++t) v[t] = base[16 * t * RS];
       if (jj > 0) {
 #pragma unroll
-        for (int m = 1; m < 8; ++m) v[m] = cmulc(v[m], __ldg(pl.tw + jj * m * 2));
+        for (int m = 1; m < 8; ++m) v[m] = cmulc(v[m], tw_at(mid_tw<N>(pl), jj * m * 2));
       }
       dftR<8, true>(v);
 #pragma unroll
@@ -1565,7 +1603,7 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
     // ---- A': inverse radix-2 stage, inverse group combine, store ----
     {
       double2 v[2][G];
-      const double2 t1 = __ldg(pl.tw + jA);
+      const double2 t1 = tw_at(mid_tw<N>(pl), jA);
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const double2 a = buf[jA * RS + g * W + wA];
@@ -1575,7 +1613,7 @@ __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(dou
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        reg_fft<G, true>(v[h], pl.tw, N);
+        reg_fft<G, true>(v[h], reg_tw<N>(pl), N);
 #pragma unroll
         for (int g = 1; g < G; ++g) v[h][g] = cmulc(v[h][g], s_tw[g * W + wA]);
         const int x0 = jA + 128 * h;
@@ -1778,7 +1816,7 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
           double2 a[G];
 #pragma unroll
           for (int g = 0; g < G; ++g) a[g] = v[g][t];
-          reg_fft<G, false>(a, pl.tw, ntab);
+          reg_fft<G, false>(a, reg_tw<N>(pl), ntab);
 #pragma unroll
           for (int g = 0; g < G; ++g) v[g][t] = a[g];
         }
@@ -1790,7 +1828,7 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
 #pragma unroll
         for (int m = 0; m < RA; ++m) {
           double2 y = v[g][m];
-          if (m > 0 && j > 0) y = cmul(y, __ldg(pl.tw + (j * m) * (ntab / N)));
+          if (m > 0 && j > 0) y = cmul(y, tw_at(mid_tw<N>(pl), (j * m) * (ntab / N)));
           dst[(j + JA * m) * RS + g * W + w] = y;
         }
       }
@@ -1810,7 +1848,7 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
       double2 v[RB];
 #pragma unroll
       for (int e = 0; e < RB; ++e) v[e] = row[e * RS];
-      reg_fft<RB, false>(v, pl.tw, ntab);
+      reg_fft<RB, false>(v, reg_tw<N>(pl), ntab);
       double rr = 0.0, rz = 0.0;
       const double wgt = s_wgt[s];
       const double al = s_alpha[c * P + pr];
@@ -1844,7 +1882,7 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
           accr[pr2] += rr;
           accz[pr2] += rz;
         }
-      reg_fft<RB, true>(v, pl.tw, ntab);
+      reg_fft<RB, true>(v, reg_tw<N>(pl), ntab);
 #pragma unroll
       for (int e = 0; e < RB; ++e) row[e * RS] = v[e];
     }
@@ -1865,7 +1903,7 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
 #pragma unroll
         for (int m = 0; m < RA; ++m) {
           double2 y = src[(j + JA * m) * RS + g * W + w];
-          if (m > 0 && j > 0) y = cmulc(y, __ldg(pl.tw + (j * m) * (ntab / N)));
+          if (m > 0 && j > 0) y = cmulc(y, tw_at(mid_tw<N>(pl), (j * m) * (ntab / N)));
           v[g][m] = y;
         }
         dftR<RA, true>(v[g]);
@@ -1876,7 +1914,7 @@ __global__ void __launch_bounds__(NT, (STG ? 1 : 512 / NT)) mid_column_reg_kerne
           double2 a[G];
 #pragma unroll
           for (int g = 0; g < G; ++g) a[g] = v[g][t];
-          reg_fft<G, true>(a, pl.tw, ntab);
+          reg_fft<G, true>(a, reg_tw<N>(pl), ntab);
 #pragma unroll
           for (int g = 0; g < G; ++g) v[g][t] = a[g];
         }
@@ -2010,8 +2048,9 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
       __syncthreads();  // barrier initialised before anyone waits
       mbar_wait(&bar, 0);
     }
-    fft_smem<NR, true, H>(buf, ColAddr{HP}, pl.tw, N);
-    c2r_pre<N>(buf, NR, HP, pl.tw);
+    const PlaneTw<N> ptw = plane_tw<N>(pl);
+    fft_smem<NR, true, H>(buf, ColAddr{HP}, ptw, N);
+    c2r_pre<N>(buf, NR, HP, ptw);
     if (MODE == INV_ITER && CHK_INV_PF_LATE && N >= CHK_INV_PF_LATE_MIN && threadIdx.x < NR) {
       // n >= 256: warm L2 with this slab's p / u rows one stage (not the whole pass)
       // before they are read -- prefetched at the start they were evicted first
@@ -2020,7 +2059,7 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
       if (do_u) bulk_prefetch_l2(u + ro, N * sizeof(double));
     }
     __syncthreads();
-    fft_smem<N2, true, NR>(buf, RowAddr{HP}, pl.tw, N);
+    fft_smem<N2, true, NR>(buf, RowAddr{HP}, ptw, N);
   }
   const double* sm = reinterpret_cast<const double*>(buf);
   constexpr int Q4 = N / 4;

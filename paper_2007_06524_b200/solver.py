@@ -208,6 +208,8 @@ def pcg_solve_batched(A, F, opts: SolveOptions | None = None, precond: Precondit
     n = batch.n
     size = n ** 3
     B = batch.B
+    if F.numel() != B * size:  # solver.py:128-130 -> operators.py:304-305
+        raise ValueError(f"load has {F.numel()} entries, expected {B} x {size}")
     Fd = F.reshape(B, size)
     if Fd.dtype != torch.float64 or Fd.device.type != "cuda":
         Fd = Fd.to("cuda", torch.float64)

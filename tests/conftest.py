@@ -36,3 +36,9 @@ def golden_configs(cfg_id):
         recs.extend(json.load(open(path))["records"])
     recs.sort(key=lambda r: r["m"])
     return recs
+
+
+@functools.lru_cache(maxsize=1)
+def golden_generic():
+    """Reference outputs at grid sizes that are not powers of two (n = 12, 20, 24, 28)."""
+    return np.load(os.path.join(GOLDEN_DIR, "generic.npz"))

@@ -8,6 +8,7 @@ records its outputs for the hot path.  The fixtures pin both the CPU oracle
     python tests/golden/make_golden.py config 3 0 16    # -> tests/golden/config3_0_16.json
     python tests/golden/make_golden.py formats          # -> tests/golden/formats.json
     python tests/golden/make_golden.py pool 3 0 256 8   # -> tests/golden/config3_full.json
+    python tests/golden/make_golden.py generic          # -> tests/golden/generic.npz (n = 12, 20, 24)
 
 Large arrays are never committed: for configs 2-5 we keep iteration counts,
 the full residual history, ||u||, <u, f>, <u, w> for a seeded Gaussian w and
@@ -300,6 +301,92 @@ def pool(cfg_id: int, start: int, count: int, workers: int):
             os.replace(path + ".tmp", path)
 
 
+def generic():
+    """Grid sizes that are not powers of two (n = n0 * L, any L; lattice.py:117-123):
+    the reference's own tests use n = 12 and 24.  Stiffness products, corrector
+    loads, the three preconditioner applies and pcg_solve runs -> generic.npz."""
+    out = {}
+    cfgs = [
+        dict(d=3, L=3, n0=4, alpha="1/4", lam=0.4, seed=21),                       # n = 12
+        dict(d=3, L=3, n0=8, alpha="1/4", lam=0.4, seed=22, subcell_offset=1),     # n = 24
+        dict(d=3, L=5, n0=4, alpha="1/2", lam=0.1, seed=23,
+             contrast=ch.ContrastModel.layered([0.1, 0.5, 0.8])),                    # n = 20
+    ]
+    for ci, kw in enumerate(cfgs):
+        kw = dict(kw)
+        seed = kw.pop("seed")
+        cfg = ch.LatticeConfig(**kw)
+        r = ch.sample_realization(cfg, seed)
+        beta = np.zeros((cfg.L,) * 3)
+        for c, b in r.cell_beta.items():
+            beta[c] = b
+        A = ch.assemble_stiffness(r)
+        x = np.random.default_rng(3000 + ci).standard_normal(cfg.n ** 3)
+        pre = f"case{ci}_"
+        out[pre + "meta"] = np.array([3, cfg.L, cfg.n0, cfg.k, cfg.offset, seed], dtype=np.int64)
+        out[pre + "lam"] = np.array(cfg.lam)
+        out[pre + "beta"] = beta
+        out[pre + "Ax"] = A.matrix() @ x
+        for i in (1, 2, 3):
+            out[pre + f"rhs{i}"] = ch.corrector_rhs(r, i)
+        print("generic case", ci, cfg.n, r.num_covered, flush=True)
+    rng = np.random.default_rng(2025)
+    for n in (12, 20):
+        t = ch.dc_correction(ch.canonical_reciprocal(ch.fourier_eigenvalues(n), 3, 1e-8))
+        x = rng.standard_normal(n ** 3)
+        out[f"lkr_x_n{n}"] = x
+        out[f"lkr_y_n{n}"] = ch.apply_lkr_preconditioner(t, x)
+        gp = ch.pseudoinverse_diag(ch.eigensum_tensor(3, ch.fourier_eigenvalues(n)))
+        out[f"fourier_y_n{n}"] = ch.apply_fourier_preconditioner(gp, x)
+        rd = regularized_inverse_diag(ch.eigensum_tensor(3, ch.fourier_eigenvalues(n)), 1e-3)
+        out[f"reg_y_n{n}"] = ch.apply_fourier_preconditioner(rd, x)
+        out[f"factors_n{n}"] = np.stack(t.factors)
+    pcg_cases = [
+        dict(L=3, n0=4, alpha="1/2", lam=0.1, seed=31, tol=1e-8, pre="lkr"),                     # n = 12
+        dict(L=3, n0=8, alpha="1/4", lam=0.4, seed=32, tol=1e-8, pre="lkr", off=1),              # n = 24
+        dict(L=5, n0=4, alpha="1/2", lam=0.05, seed=33, tol=1e-10, pre="fourier", rhs="noise"),  # n = 20
+        dict(L=6, n0=4, alpha="1/2", lam=0.01, seed=34, tol=1e-9, pre="regularized"),            # n = 24
+        dict(L=3, n0=4, alpha="1/4", lam=0.4, seed=35, tol=1e-9, pre="lkr", prs=True),           # n = 12
+        dict(L=7, n0=4, alpha="1/2", lam=0.1, seed=36, tol=1e-30, pre="lkr", max_iter=4),        # n = 28
+    ]
+    for pi, kw in enumerate(pcg_cases):
+        cfg = ch.LatticeConfig(d=3, L=kw["L"], n0=kw["n0"], alpha=kw["alpha"], lam=kw["lam"],
+                               subcell_offset=kw.get("off"))
+        r = ch.sample_realization(cfg, kw["seed"])
+        A = ch.assemble_stiffness(r)
+        h = 1.0 / cfg.n
+        if kw.get("rhs") == "noise":
+            # a load with a non-zero mean: pcg_solve projects it (solver.py:139-143)
+            f = np.random.default_rng(kw["seed"]).standard_normal(cfg.n ** 3) + 0.25
+        else:
+            f = (h ** (2 - 3)) * ch.corrector_rhs(r, 1)
+        opts = ch.SolveOptions(tol=kw["tol"], preconditioner=kw["pre"], eps_rank=1e-8,
+                               delta=1e-3 if kw["pre"] == "regularized" else 0.0,
+                               precond_residual_stopping=kw.get("prs", False),
+                               max_iter=kw.get("max_iter", 500))
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            u, rep = ch.pcg_solve(A, f, opts)
+        beta = np.zeros((cfg.L,) * 3)
+        for c, b in r.cell_beta.items():
+            beta[c] = b
+        pre = f"pcg{pi}_"
+        out[pre + "meta"] = np.array([cfg.L, cfg.n0, cfg.k, cfg.offset, rep.iterations, int(rep.converged),
+                                      int(kw.get("prs", False)), kw.get("max_iter", 500),
+                                      int(rep.rhs_projected)], dtype=np.int64)
+        out[pre + "lam_tol"] = np.array([cfg.lam, kw["tol"]])
+        out[pre + "kind"] = np.array(kw["pre"])
+        out[pre + "beta"] = beta
+        out[pre + "f"] = f
+        out[pre + "u"] = u
+        out[pre + "res"] = np.array(rep.residuals)
+        out[pre + "name"] = np.array(rep.preconditioner)
+        print("generic pcg", pi, cfg.n, rep.iterations, rep.converged, rep.preconditioner, rep.rhs_projected, flush=True)
+    np.savez_compressed(os.path.join(HERE, "generic.npz"), **out)
+    print("wrote generic.npz", os.path.getsize(os.path.join(HERE, "generic.npz")))
+
+
 def formats():
     """Wire formats around the path: realization JSON
     (lattice.py:229-250) for every contrast kind / offset, and the CSV cell
@@ -337,6 +424,8 @@ if __name__ == "__main__":
         small()
     elif sys.argv[1] == "formats":
         formats()
+    elif sys.argv[1] == "generic":
+        generic()
     elif sys.argv[1] == "pool":
         pool(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]))
     else:

@@ -291,9 +291,9 @@ def test_size_mismatch_raises_value_error():
     t = chk.dc_correction(chk.canonical_reciprocal(chk.fourier_eigenvalues(8), 3, 1e-8))
     with pytest.raises(ValueError):
         chk.apply_lkr_preconditioner(t, np.ones(10))
-    cfg = chk.LatticeConfig(d=3, L=3, n0=4, lam=0.4)  # n = 12: not a power of two
+    cfg = chk.LatticeConfig(d=3, L=3, n0=4, lam=0.4)  # n = 12 (generic path): wrong load size
     with pytest.raises(ValueError):
-        chk.pcg_solve(chk.assemble_stiffness(chk.sample_realization(cfg, 1)), np.ones(12 ** 3))
+        chk.pcg_solve(chk.assemble_stiffness(chk.sample_realization(cfg, 1)), np.ones(12 ** 3 + 1))
 
 
 @pytest.mark.parametrize("hid", _case_ids("homog"))

@@ -157,3 +157,64 @@ def test_oracle_config2_first_realization():
     assert rep.iterations == rec["iterations"]
     assert np.allclose(rep.residuals, rec["residuals"], rtol=1e-8, atol=0)
     assert abs(np.linalg.norm(u) - rec["norm_u"]) <= 1e-9 * rec["norm_u"]
+
+
+# ---- grid sizes that are not powers of two (generic.npz: n = 12, 20, 24, 28) -------------
+def _generic_ids(prefix):
+    from conftest import golden_generic
+    g = golden_generic()
+    return sorted({k.split("_")[0] for k in g.files if k.startswith(prefix)})
+
+
+@pytest.mark.parametrize("case", _generic_ids("case"))
+def test_oracle_generic_stencil_rhs(case):
+    from conftest import golden_generic
+    g = golden_generic()
+    d, L, n0, k, off, _ = (int(v) for v in g[case + "_meta"])
+    F = orc.cell_field(g[case + "_beta"], n0, k, off)
+    n = n0 * L
+    x = np.random.default_rng(3000 + int(case[4:])).standard_normal(n ** 3)
+    ref = g[case + "_Ax"]
+    assert np.linalg.norm(orc.stencil_apply(F, float(g[case + "_lam"]), x) - ref) <= 1e-14 * np.linalg.norm(ref)
+    for i in (1, 2, 3):
+        assert np.allclose(orc.corrector_rhs(F, i), g[case + f"_rhs{i}"], rtol=0, atol=1e-17)
+
+
+@pytest.mark.parametrize("n", [12, 20])
+def test_oracle_generic_preconditioners(n):
+    from conftest import golden_generic
+    g = golden_generic()
+    x = g[f"lkr_x_n{n}"]
+    fac = orc.lkr_factors(n)
+    assert np.array_equal(fac, g[f"factors_n{n}"])
+    ref = g[f"lkr_y_n{n}"]
+    assert np.linalg.norm(orc.apply_lkr(fac, x) - ref) <= 1e-14 * np.linalg.norm(ref)
+    yf = orc.apply_fourier(orc.pseudoinverse_diag(n), x)
+    assert np.linalg.norm(yf - g[f"fourier_y_n{n}"]) <= 1e-14 * np.linalg.norm(yf)
+    yr = orc.apply_fourier(orc.pseudoinverse_diag(n, delta=1e-3), x)
+    assert np.linalg.norm(yr - g[f"reg_y_n{n}"]) <= 1e-14 * np.linalg.norm(yr)
+
+
+@pytest.mark.parametrize("pid", _generic_ids("pcg"))
+def test_oracle_generic_pcg(pid):
+    from conftest import golden_generic
+    g = golden_generic()
+    L, n0, k, off, its, conv, prs, max_iter, proj = (int(v) for v in g[pid + "_meta"])
+    lam, tol = (float(v) for v in g[pid + "_lam_tol"])
+    kind = str(g[pid + "_kind"])
+    F = orc.cell_field(g[pid + "_beta"], n0, k, off)
+    n = n0 * L
+    if kind == "lkr":
+        fac = orc.lkr_factors(n)
+        dg = orc.lkr_diagonal(fac)
+        P = lambda x: orc.apply_lkr(fac, x, dg)  # noqa: E731
+    else:
+        dg = orc.pseudoinverse_diag(n, delta=1e-3 if kind == "regularized" else 0.0)
+        P = lambda x: orc.apply_fourier(dg, x)  # noqa: E731
+    A = orc.StencilMatrix(F, lam)
+    u, rep = orc.pcg_solve(A.__matmul__, g[pid + "_f"], P, tol=tol, max_iter=max_iter,
+                           precond_residual_stopping=bool(prs))
+    assert rep.iterations == its and rep.converged == bool(conv)
+    assert np.allclose(rep.residuals, g[pid + "_res"], rtol=1e-8, atol=0)
+    uref = g[pid + "_u"]
+    assert np.linalg.norm(u - uref) <= 1e-9 * np.linalg.norm(uref)
