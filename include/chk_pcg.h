@@ -15,8 +15,13 @@
  *   CHK_OK           0
  *   CHK_EINVAL       1  bad argument / size mismatch      -> ValueError
  *                       (operators.py:304-305, spectral.py:107-108, lowrank.py:187-188)
- *   CHK_EUNSUPPORTED 2  unsupported grid (d != 3, n not a power of two in
- *                       [8, 512])                        -> ValueError
+ *   CHK_EUNSUPPORTED 2  unsupported grid (d != 3; n not n0*L with n <= 720;
+ *                       slab entry points: n not a power of two in [8, 512])
+ *                                                         -> ValueError
+ * Grid sizes: n = n0*L with n0 a power of two >= 4 and any L >= 1, as the
+ * reference (lattice.py:117-123,156-159).  Powers of two 8..512 (the BASELINE
+ * configurations) run the fused kernels; every other n <= 720 (e.g. 12, 20,
+ * 24, 96) runs plain device kernels with the same semantics and results.
  *   CHK_ECUDA        3  CUDA runtime failure              -> RuntimeError
  * chk_last_error() returns a thread-local message for the last failure.
  *

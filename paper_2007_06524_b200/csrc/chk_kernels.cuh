@@ -896,7 +896,8 @@ template <int N>
 __device__ __forceinline__ PlaneTw<N> plane_tw(const PlanDev& pl) { return TwSel<N, (CHK_CTW != 0 && N <= 256)>::get(pl); }
 // middle passes: register FFTs (reg_fft) index the table with compile-time constants,
 // which become constant-bank operands of the multiplies (no load instruction at all):
-// reg_tw.  Stages whose twiddle index varies inside a warp keep the global table
+// reg_tw (n = 128 middle pass -3.7 %, n = 256 -6 %; n = 512, register-capped at 128 and
+// latency-bound, +8 %, so it keeps the table).  Stages whose twiddle index varies inside a warp keep the global table
 // (divergent constant loads replay: n = 128 middle pass +30 %, n = 512 +12 % when tried),
 // except in the n = 256 register-phase kernel, where every twiddle from constant memory
 // measured -6 % (mid_tw).
@@ -904,9 +905,9 @@ __device__ __forceinline__ PlaneTw<N> plane_tw(const PlanDev& pl) { return TwSel
 #define CHK_CTW_MID 1
 #endif
 template <int N>
-using RegTw = typename TwSel<N, (CHK_CTW_MID != 0)>::type;
+using RegTw = typename TwSel<N, (CHK_CTW_MID != 0 && N <= 256)>::type;
 template <int N>
-__device__ __forceinline__ RegTw<N> reg_tw(const PlanDev& pl) { return TwSel<N, (CHK_CTW_MID != 0)>::get(pl); }
+__device__ __forceinline__ RegTw<N> reg_tw(const PlanDev& pl) { return TwSel<N, (CHK_CTW_MID != 0 && N <= 256)>::get(pl); }
 template <int N>
 using MidTw = typename TwSel<N, (CHK_CTW_MID != 0 && N == 256)>::type;
 template <int N>
