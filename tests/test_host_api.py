@@ -40,7 +40,10 @@ def test_library_is_sm100a():
 def test_abi_rejects_bad_arguments_without_gpu():
     lib = _lib.load()
     h = ctypes.c_void_p()
-    assert lib.chk_precond_plan_create(1, 12, 5, None, None, 0.0, ctypes.byref(h)) == _lib.CHK_EUNSUPPORTED
+    # n = 12 runs the generic kernels; 724 (> 720, not a power of two) and 10 (not n0 * L) do not exist
+    assert lib.chk_precond_plan_create(1, 724, 5, None, None, 0.0, ctypes.byref(h)) == _lib.CHK_EUNSUPPORTED
+    assert lib.chk_precond_plan_create(1, 10, 5, None, None, 0.0, ctypes.byref(h)) == _lib.CHK_EUNSUPPORTED
+    assert lib.chk_precond_plan_create(1, 12, 5, None, None, 0.0, ctypes.byref(h)) == _lib.CHK_EINVAL  # no factors
     assert lib.chk_precond_plan_create(7, 16, 5, None, None, 0.0, ctypes.byref(h)) == _lib.CHK_EINVAL
     g = _lib.ChkGrid(2, 16, 4, 4, 2, 1, 0.4)
     assert lib.chk_stencil_apply(ctypes.byref(g), None, None, None, None, 1, None) == _lib.CHK_EUNSUPPORTED
