@@ -291,7 +291,7 @@ struct Ops {
     } else if (N == 256 && CHK_R256) {
       // register-phase kernel (x0 radix order 2, 8, 8, 2; diagonal from the plan table)
       if (!pl.D) return fail(CHK_EINVAL, "n = 256 middle pass needs the plan's diagonal table");
-      const size_t sm = (size_t)N * (G * W + 1) * sizeof(double2);
+      const size_t sm = (size_t)N * CHK_R256_RS * sizeof(double2);
       CHK_CUDA(allow_smem(mid_column_r256_kernel<NBX, MODE>, sm));
       mid_column_r256_kernel<NBX, MODE><<<grid, 256, sm, s>>>(S, pl, ctl, sg, it, B);
     } else if (pl.D && mid_dg()) {

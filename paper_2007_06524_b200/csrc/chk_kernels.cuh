@@ -1466,12 +1466,18 @@ template <int NB, int MODE>
 #ifndef CHK_R256_RPF
 #define CHK_R256_RPF 1
 #endif
+#ifndef CHK_R256_RS
+#define CHK_R256_RS 18
+#endif
 #ifndef CHK_R256_MINB
 #define CHK_R256_MINB 2
 #endif
 __global__ void __launch_bounds__(256, CHK_R256_MINB) mid_column_r256_kernel(double2* __restrict__ S, PlanDev pl, SolveCtl ctl,
                                                                  SlabGeo sg, int it, int B) {
-  constexpr int N = 256, G = 8, W = 2, GW = G * W, RS = GW + 1;
+  // row pitch 18: phase A / A' lanes hold (x0 pair, column) = (lane >> 1, lane & 1), so a
+  // quarter warp touches {0, 1} + pitch * {0..3}: distinct 16-byte banks need pitch = 2 mod 8
+  // (pitch 17 was a 2-way conflict on those four accesses: 34 M of 179 M wavefronts per launch)
+  constexpr int N = 256, G = 8, W = 2, GW = G * W, RS = CHK_R256_RS;
   static_assert(IlW<N>::value == W, "interleaved spectrum layout expected at n = 256");
   static_assert(x0_radix(N, 256) == 2 && x0_radix(N, 128) == 8 && x0_radix(N, 16) == 8 && x0_radix(N, 2) == 2,
                 "x0 radix order 2, 8, 8, 2");
