@@ -55,6 +55,9 @@
 #ifndef CHK_SC_FENCE
 #define CHK_SC_FENCE 0
 #endif
+#ifndef CHK_U_TMA  // n = 128 inverse pass: u += alpha p as a TMA bulk reduce-add from shared memory
+#define CHK_U_TMA 1
+#endif
 
 namespace chk {
 
@@ -2068,8 +2071,15 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
     __syncthreads();
     fft_smem<N2, true, NR>(buf, RowAddr{HP}, ptw, N);
   }
-  const double* sm = reinterpret_cast<const double*>(buf);
+  double* sm = reinterpret_cast<double*>(buf);
   constexpr int Q4 = N / 4;
+  // u += alpha p by the TMA engine (n = 128, where this pass is LSU-bound; measured: pair
+  // pass -3.0 %, config 3 +2.1 %; the HBM-bound n = 64 pass +1.3 %): alpha p replaces the z quad this thread has
+  // just read in the shared-memory row, and one bulk reduce-add per row (cp.reduce.async.bulk
+  // .add.f64, performed at the L2) accumulates it into u -- the LSU pipe, which bounds this
+  // pass, moves 8 instead of 16 wavefronts per row for u.  (alpha p is rounded before the
+  // add, as in the reference's own `u += alpha * p`, solver.py:167.)
+  constexpr bool UTMA = CHK_U_TMA && MODE == INV_ITER && N == 128;
   for (int i = threadIdx.x; i < NR * Q4; i += blockDim.x) {
     const int t = i / Q4, x2 = 4 * (i - (i / Q4) * Q4);
     const size_t idx = b * nb + ((size_t)x0 * N + gg + G * t) * N + x2;
@@ -2083,16 +2093,35 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
       double po[4], uo[4];
       ldv4(out + idx, po);
       if (do_u) {
-        ldv4(u + idx, uo);
+        if constexpr (UTMA) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) uo[e] = fma(alpha, po[e], uo[e]);  // u += step p
-        stv4(u + idx, uo);
+          for (int e = 0; e < 4; ++e) uo[e] = alpha * po[e];
+          st_quad_smem(sm + t * 2 * HP, x2, uo);
+        } else {
+          ldv4(u + idx, uo);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) uo[e] = fma(alpha, po[e], uo[e]);  // u += step p
+          stv4(u + idx, uo);
+        }
       }
       if (do_p) {
         double pn[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) pn[e] = fma(beta, po[e], z[e]);  // p = z + beta p
         stv4(out + idx, pn);
+      }
+    }
+  }
+  if constexpr (UTMA) {
+    if (do_u) {  // CTA-uniform
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x < NR) {
+        const int t = threadIdx.x;
+        bulk_reduce_add_f64(u + b * nb + ((size_t)x0 * N + gg + G * t) * N, sm + t * 2 * HP,
+                            (uint32_t)(N * sizeof(double)));
+        bulk_commit();
+        bulk_wait_read0();
       }
     }
   }

@@ -57,6 +57,13 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src_smem, uint32
                "r"(smem_u32(src_smem)), "r"(bytes)
                : "memory");
 }
+// global[0..bytes) += shared[0..bytes) as doubles, performed by the TMA engine / L2
+// (cp.reduce.async.bulk ... .add.f64; bulk-group completion)
+__device__ __forceinline__ void bulk_reduce_add_f64(double* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src_smem)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
