@@ -2074,7 +2074,8 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
   double* sm = reinterpret_cast<double*>(buf);
   constexpr int Q4 = N / 4;
   // u += alpha p by the TMA engine (n = 128, where this pass is LSU-bound; measured: pair
-  // pass -3.0 %, config 3 +2.1 %; the HBM-bound n = 64 pass +1.3 %): alpha p replaces the z quad this thread has
+  // pass -3.0 %, config 3 +2.1 %; the HBM- or latency-bound passes of the other sizes lose:
+  // n = 64 +1.3 %, n = 256 +9 %, n = 512 +4 %): alpha p replaces the z quad this thread has
   // just read in the shared-memory row, and one bulk reduce-add per row (cp.reduce.async.bulk
   // .add.f64, performed at the L2) accumulates it into u -- the LSU pipe, which bounds this
   // pass, moves 8 instead of 16 wavefronts per row for u.  (alpha p is rounded before the
