@@ -5,8 +5,8 @@ pattern; after the call the guards must be intact (no out-of-bounds write), the
 inputs unchanged, and a workspace pre-filled with NaN garbage must give the
 bit-identical result of a zeroed one (no read of memory the kernels did not
 write first).  Covers every grid size of the path, the paired n = 128 schedule,
-the fused n >= 256 middle passes, the stand-alone operators and the host
-pipeline."""
+the fused n >= 256 middle passes, the generic kernels of the other sizes, the
+stand-alone operators and the host pipeline."""
 
 import numpy as np
 import pytest
@@ -63,7 +63,8 @@ class GuardedWorkspace(solver.Workspace):
 
 
 CASES = [(2, 4, 0.1, 3, 1e-8), (4, 4, 0.1, 3, 1e-8), (8, 4, 0.1, 2, 1e-8), (16, 4, 0.1, 4, 1e-8),
-         (32, 4, 0.01, 40, 1e-8), (64, 4, 0.1, 2, 1e-10), (32, 16, 0.1, 1, 1e-8)]
+         (32, 4, 0.01, 40, 1e-8), (64, 4, 0.1, 2, 1e-10), (32, 16, 0.1, 1, 1e-8),
+         (3, 4, 0.1, 3, 1e-8), (5, 8, 0.1, 2, 1e-8), (1, 4, 0.1, 2, 1e-8)]  # generic sizes n = 12, 40, 4
 
 
 @pytest.mark.parametrize("L,n0,lam,B,tol", CASES, ids=[f"n{L * n0}xB{B}" for L, n0, lam, B, tol in CASES])
@@ -91,7 +92,7 @@ def test_solver_guards_and_poisoned_workspace(L, n0, lam, B, tol):
     assert np.array_equal(results[0][1], results[1][1]) and np.array_equal(results[0][2], results[1][2])
 
 
-@pytest.mark.parametrize("n", [16, 64, 128, 256, 512])
+@pytest.mark.parametrize("n", [16, 64, 128, 256, 512, 12, 36])
 def test_operators_guards(n):
     import ctypes
 
