@@ -522,8 +522,34 @@ Workspace carve(void* base, int n, int B, int max_iter) {
 struct PinnedStates {
   RState* h = nullptr;
   size_t cap = 0;
+  int* flags = nullptr;  // [2] "any realization still active" words written by poll_active_kernel
   ~PinnedStates() {
     if (h) cudaFreeHost(h);
+    if (flags) cudaFreeHost(flags);
+    if (hist) cudaFreeHost(hist);
+  }
+  // Host-mapped words for the convergence poll.  The device writes them itself (zero-copy
+  // store from a one-CTA kernel) instead of a cudaMemcpyAsync: a status copy queues on the
+  // device-to-host copy engine behind any bulk download in flight (another pipeline lane's
+  // 0.5 GB of solutions, ~10 ms), the polling host thread then waits that long, and with
+  // only a few iterations of look-ahead queued the GPU ran dry (a 4 GiB download beside a
+  // config-3 solve cost 50 ms this way).
+  int* poll_flags() {
+    if (!flags && cudaHostAlloc(&flags, 64, cudaHostAllocMapped) != cudaSuccess) flags = nullptr;
+    return flags;
+  }
+  // pinned staging of the residual histories (same reason: written by the device itself)
+  double* hist = nullptr;
+  size_t hist_cap = 0;
+  double* get_hist(size_t n) {
+    if (n > hist_cap) {
+      if (hist) cudaFreeHost(hist);
+      hist = nullptr;
+      hist_cap = 0;
+      if (cudaMallocHost(&hist, n * sizeof(double)) != cudaSuccess) return hist = nullptr;
+      hist_cap = n;
+    }
+    return hist;
   }
   RState* get(size_t n) {
     if (n > cap) {
@@ -540,6 +566,61 @@ struct PinnedStates {
   }
 };
 thread_local PinnedStates g_pinned;
+
+// n 8-byte words device -> pinned host memory by zero-copy stores (small read-backs that must
+// not queue behind bulk downloads on the copy engine)
+__global__ void words_to_host_kernel(const unsigned long long* __restrict__ src, unsigned long long* dst, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  __threadfence_system();
+}
+
+// out[0] = 1 while any realization is still active (host-mapped memory, see poll_flags)
+__global__ void poll_active_kernel(const RState* __restrict__ st, int B, int* out) {
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  int a = 0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) a |= (st[b].status == ST_ACTIVE);
+  if (a) any = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *out = any;
+    __threadfence_system();
+  }
+}
+
+// Per-realization states (and optionally the residual histories) back to the host after a
+// solve: zero-copy kernels into pinned memory, one stream synchronize, then plain host copies.
+static_assert(sizeof(RState) % 8 == 0, "RState is copied as 8-byte words");
+int read_back(const Workspace& w, int B, int max_iter, int32_t* iterations, double* final_rel, int32_t* status,
+              int32_t* rhs_projected, double* history, cudaStream_t s) {
+  RState* hst = g_pinned.get((size_t)B);
+  if (!hst) return fail(CHK_ECUDA, "cudaMallocHost failed");
+  words_to_host_kernel<<<4, 256, 0, s>>>(reinterpret_cast<const unsigned long long*>(w.st),
+                                        reinterpret_cast<unsigned long long*>(hst), sizeof(RState) / 8 * (size_t)B);
+  CHK_LAUNCHED();
+  double* hh = nullptr;
+  const size_t nh = (size_t)max_iter * B;
+  if (history) {
+    hh = g_pinned.get_hist(nh);
+    if (!hh) return fail(CHK_ECUDA, "cudaMallocHost failed");
+    words_to_host_kernel<<<32, 256, 0, s>>>(reinterpret_cast<const unsigned long long*>(w.hist),
+                                           reinterpret_cast<unsigned long long*>(hh), nh);
+    CHK_LAUNCHED();
+  }
+  CHK_CUDA(cudaStreamSynchronize(s));
+  if (history) memcpy(history, hh, sizeof(double) * nh);
+  for (int b = 0; b < B; ++b) {
+    int stt = hst[b].status;
+    if (stt == ST_ACTIVE) stt = ST_NOT_CONVERGED;  // defensive; max_iter always decides
+    if (status) status[b] = stt;
+    if (iterations) iterations[b] = hst[b].iters;
+    if (final_rel) final_rel[b] = hst[b].final_rel;
+    if (rhs_projected) rhs_projected[b] = hst[b].rhs_projected;
+  }
+  return CHK_OK;
+}
 
 // ---- generic grid sizes (chk_generic.cuh) ----
 // z = P x for the B complex arrays already in S (x + 0 i): forward sums along x2,
@@ -574,8 +655,8 @@ int gen_solve(const Geo& g, const PlanDev& pl, const double* beta, const double*
   const dim3 grid(n, B);
   SolveCtl ctl{w.st, nullptr, w.part, w.hist, n, opts->max_iter, opts->tol, opts->precond_residual_stopping ? 1 : 0,
                w.red, 0};
-  RState* hst_all = g_pinned.get((size_t)2 * B);
-  if (!hst_all) return fail(CHK_ECUDA, "cudaMallocHost failed");
+  int* flags = g_pinned.poll_flags();
+  if (!flags) return fail(CHK_ECUDA, "cudaMallocHost failed");
   CHK_CUDA(cudaMemsetAsync(w.st, 0, sizeof(RState) * B, s));
   CHK_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(double) * (size_t)opts->max_iter * B, s));
   CHK_CUDA(cudaMemsetAsync(w.red, 0, sizeof(double) * 4 * B, s));
@@ -631,12 +712,10 @@ int gen_solve(const Geo& g, const PlanDev& pl, const double* beta, const double*
       if (it % chunk == 0 || it == opts->max_iter) {
         if (pending) {
           CHK_CUDA(cudaEventSynchronize(ev[ev_i ^ 1]));
-          const RState* prev = hst_all + (size_t)(ev_i ^ 1) * B;
-          bool any = false;
-          for (int b = 0; b < B; ++b) any |= (prev[b].status == ST_ACTIVE);
-          if (!any) break;
+          if (!reinterpret_cast<volatile int*>(flags)[ev_i ^ 1]) break;
         }
-        CHK_CUDA(cudaMemcpyAsync(hst_all + (size_t)ev_i * B, w.st, sizeof(RState) * B, cudaMemcpyDeviceToHost, s));
+        poll_active_kernel<<<1, 256, 0, s>>>(w.st, B, flags + ev_i);
+        CHK_LAUNCHED();
         CHK_CUDA(cudaEventRecord(ev[ev_i], s));
         ev_i ^= 1;
         pending = true;
@@ -655,20 +734,7 @@ int gen_solve(const Geo& g, const PlanDev& pl, const double* beta, const double*
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
   if (rc) return rc;
-  RState* hst = hst_all;
-  CHK_CUDA(cudaMemcpyAsync(hst, w.st, sizeof(RState) * B, cudaMemcpyDeviceToHost, s));
-  if (history)
-    CHK_CUDA(cudaMemcpyAsync(history, w.hist, sizeof(double) * (size_t)opts->max_iter * B, cudaMemcpyDeviceToHost, s));
-  CHK_CUDA(cudaStreamSynchronize(s));
-  for (int b = 0; b < B; ++b) {
-    int stt = hst[b].status;
-    if (stt == ST_ACTIVE) stt = ST_NOT_CONVERGED;
-    if (status) status[b] = stt;
-    if (iterations) iterations[b] = hst[b].iters;
-    if (final_rel) final_rel[b] = hst[b].final_rel;
-    if (rhs_projected) rhs_projected[b] = hst[b].rhs_projected;
-  }
-  return CHK_OK;
+  return read_back(w, B, opts->max_iter, iterations, final_rel, status, rhs_projected, history, s);
 }
 
 }  // namespace
@@ -980,9 +1046,8 @@ int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const
     return gen_solve(g, pl, beta, f, u, B, opts, iterations, final_rel, status, rhs_projected, history, w, s);
   SolveCtl ctl{w.st, w.Rh, w.part, w.hist, maxblk_of(n), opts->max_iter, opts->tol,
                opts->precond_residual_stopping ? 1 : 0, nullptr, 0};
-  RState* hst_all = g_pinned.get((size_t)2 * B);
-  RState* hst = hst_all;
-  if (!hst_all) return fail(CHK_ECUDA, "cudaMallocHost failed");
+  int* flags = g_pinned.poll_flags();
+  if (!flags) return fail(CHK_ECUDA, "cudaMallocHost failed");
   CHK_CUDA(cudaMemsetAsync(w.st, 0, sizeof(RState) * B, s));
   CHK_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(double) * (size_t)opts->max_iter * B, s));
 
@@ -1008,16 +1073,13 @@ int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const
         if (it % chunk == 0 || it == opts->max_iter) {
           if (pending) {
             CHK_CUDA(cudaEventSynchronize(ev[ev_i ^ 1]));
-            const RState* prev = hst_all + (size_t)(ev_i ^ 1) * B;
-            bool any = false;
-            for (int b = 0; b < B; ++b) any |= (prev[b].status == ST_ACTIVE);
-            if (!any) {
+            if (!reinterpret_cast<volatile int*>(flags)[ev_i ^ 1]) {
               stop = true;
               return CHK_OK;
             }
           }
-          CHK_CUDA(cudaMemcpyAsync(hst_all + (size_t)ev_i * B, w.st, sizeof(RState) * B,
-                                   cudaMemcpyDeviceToHost, s));
+          poll_active_kernel<<<1, 256, 0, s>>>(w.st, B, flags + ev_i);
+          CHK_LAUNCHED();
           CHK_CUDA(cudaEventRecord(ev[ev_i], s));
           ev_i ^= 1;
           pending = true;
@@ -1091,21 +1153,9 @@ int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
   if (rc) return rc;
-  CHK_CUDA(cudaMemcpyAsync(hst, w.st, sizeof(RState) * B, cudaMemcpyDeviceToHost, s));
-  if (history)
-    CHK_CUDA(cudaMemcpyAsync(history, w.hist, sizeof(double) * (size_t)opts->max_iter * B,
-                             cudaMemcpyDeviceToHost, s));
-  CHK_CUDA(cudaStreamSynchronize(s));
+  rc = read_back(w, B, opts->max_iter, iterations, final_rel, status, rhs_projected, history, s);
   g_prof.collect();
-  for (int b = 0; b < B; ++b) {
-    int stt = hst[b].status;
-    if (stt == ST_ACTIVE) stt = ST_NOT_CONVERGED;  // defensive; max_iter always decides
-    if (status) status[b] = stt;
-    if (iterations) iterations[b] = hst[b].iters;
-    if (final_rel) final_rel[b] = hst[b].final_rel;
-    if (rhs_projected) rhs_projected[b] = hst[b].rhs_projected;
-  }
-  return CHK_OK;
+  return rc;
 }
 
 }  // namespace
@@ -1254,22 +1304,14 @@ int host_pipeline(const chk_grid* grid, const chk_precond_plan* plan, const Pipe
       }
       const int rc = solve_batched_impl(grid, plan, d_b, d_f, d_u, nbc, opts, iterations ? iterations + b0 : nullptr,
                                         final_rel ? final_rel + b0 : nullptr, status ? status + b0 : nullptr,
-                                        rhs_projected ? rhs_projected + b0 : nullptr, nullptr, solver_ws,
+                                        rhs_projected ? rhs_projected + b0 : nullptr,
+                                        history ? history + (size_t)opts->max_iter * b0 : nullptr, solver_ws,
                                         solver_bytes, ls);
       o.launches += g_launches;
       if (rc) {
         o.rc = rc;
         o.err = g_err;
         break;
-      }
-      if (history) {
-        // chk_pcg_solve_batched keeps the device history inside its workspace: copy it out
-        Workspace w = carve(solver_ws, grid->n, nbc, opts->max_iter);
-        if ((e = cudaMemcpyAsync(history + (size_t)opts->max_iter * b0, w.hist, sizeof(double) * opts->max_iter * nbc,
-                                 cudaMemcpyDeviceToHost, ls))) {
-          bad(CHK_ECUDA, "history copy", e);
-          break;
-        }
       }
       if ((e = cudaMemcpyAsync(u_host + nb * b0, d_u, sizeof(double) * nb * nbc, cudaMemcpyDeviceToHost, ls))) {
         bad(CHK_ECUDA, "download", e);
