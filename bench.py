@@ -321,7 +321,7 @@ def run_ours(args):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        step_seeds = [chk.derive_seed(0, m) for m in range(lo, hi)]  # the host work of the step
+        step_seeds = chk.derive_seeds(0, range(lo, hi))  # the host work of the step (SeedSequence hashes)
         res_e = chk.pcg_solve_seeds(lat, step_seeds, opts, P, rhs=f_h if f_h is not None else 1, out=U_h,
                                     record_history=False, workspace=ws_h, chunk=args.e2e_chunk or None)
         t1.record(stream)

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <exception>
 #include <string>
 #include <thread>
@@ -1226,8 +1227,26 @@ int host_pipeline(const chk_grid* grid, const chk_precond_plan* plan, const Pipe
   const size_t data_bytes = align_up(sizeof(double) * (2 * nb + lb) * chunk);
   const size_t slot_bytes = data_bytes + align_up(2 * sizeof(uint64_t) * chunk);
   const size_t solver_bytes = align_up(chk_pcg_workspace_bytes(grid, plan, chunk, opts->max_iter));
-  const int nchunks = (B + chunk - 1) / chunk;
-  const int lanes = host_lanes(nchunks);
+  // Chunk schedule: full chunks while more than a round of them remains, then halved and
+  // quartered chunks, handed to whichever lane is free -- the lanes finish together and
+  // the last download, which nothing can overlap, is a quarter chunk (CHK_HOST_TAPER=0:
+  // equal chunks, round-robin as before).
+  static const bool taper = !(getenv("CHK_HOST_TAPER") && atoi(getenv("CHK_HOST_TAPER")) == 0);
+  const int lanes = host_lanes((B + chunk - 1) / chunk);
+  std::vector<std::pair<int, int>> sched;  // (first realization, count)
+  for (int b0 = 0; b0 < B;) {
+    int c = chunk;
+    if (taper) {
+      const int rem = B - b0;
+      if (rem <= lanes * chunk / 2 && chunk >= 4) c = chunk / 4;
+      else if (rem <= lanes * chunk && chunk >= 2) c = chunk / 2;
+    }
+    c = std::min(c, B - b0);
+    sched.push_back({b0, c});
+    b0 += c;
+  }
+  const int nchunks = (int)sched.size();
+  std::atomic<int> next_chunk{0};
   const double h = 1.0 / grid->n;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = 0;
@@ -1259,8 +1278,8 @@ int host_pipeline(const chk_grid* grid, const chk_precond_plan* plan, const Pipe
     uint64_t* d_k = reinterpret_cast<uint64_t*>(base + data_bytes);
     void* solver_ws = base + slot_bytes;
     if ((e = cudaStreamWaitEvent(ls, start, 0)) != cudaSuccess) bad(CHK_ECUDA, "lane wait", e);
-    for (int c = lane; c < nchunks && o.rc == CHK_OK; c += lanes) {
-      const int b0 = c * chunk, nbc = (B - b0 < chunk) ? B - b0 : chunk;
+    for (int c = next_chunk.fetch_add(1); c < nchunks && o.rc == CHK_OK; c = next_chunk.fetch_add(1)) {
+      const int b0 = sched[c].first, nbc = sched[c].second;
       if (in.beta_host) {
         if ((e = cudaMemcpyAsync(d_b, in.beta_host + lb * b0, sizeof(double) * lb * nbc, cudaMemcpyHostToDevice, ls))) {
           bad(CHK_ECUDA, "upload beta", e);

@@ -208,3 +208,23 @@ def test_no_oracle_import_in_product():
                 text = open(os.path.join(root, fn)).read()
                 assert "oracle" not in re.sub(r"#.*", "", text).split("\"\"\"")[-1] or "import oracle" not in text
                 assert "from oracle" not in text and "import oracle" not in text
+
+
+def test_vectorised_seed_hashing_is_numpy_seedsequence():
+    """derive_seeds / philox_keys (the host work of the seeds pipeline, hashed for the whole
+    batch at once) against numpy's SeedSequence and the reference's golden seeds."""
+    from conftest import golden_small
+
+    g = golden_small()
+    assert np.array_equal(chk.derive_seeds(0, range(256)), g["seeds_master0"])
+    assert np.array_equal(chk.derive_seeds(7, range(16)), g["seeds_master7"])
+    for master in (0, 3, 2 ** 40 + 3, 12345678901234567890123):
+        idx = list(range(40)) + [65536, 2 ** 31, 2 ** 32 - 1]
+        ref = [chk.derive_seed(master, m) for m in idx]
+        assert [int(v) for v in chk.derive_seeds(master, idx)] == ref
+    assert int(chk.derive_seeds(5, [2 ** 32 + 1])[0]) == chk.derive_seed(5, 2 ** 32 + 1)  # numpy fallback
+    rng = np.random.default_rng(3)
+    seeds = [int(v) for v in rng.integers(0, 2 ** 63, size=200, dtype=np.uint64)] + [0, 1, 2 ** 32 - 1, 2 ** 32, 2 ** 64 - 1]
+    ref = np.stack([np.random.SeedSequence(s).generate_state(2, np.uint64) for s in seeds])
+    from paper_2007_06524_b200.lattice import philox_keys
+    assert np.array_equal(philox_keys(seeds), ref)
