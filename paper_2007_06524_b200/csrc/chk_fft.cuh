@@ -82,9 +82,43 @@ __device__ __forceinline__ void dft8(double2 (&v)[8]) {
   v[3] = cadd(a3, b3); v[7] = csub(a3, b3);
 }
 
+// y_k = sum_t v_t w16^{tk}, natural order in and out: 16 = 4 x 4 (t = 4a + b, k = m + 4n),
+// y[m + 4n] = sum_b w4^{bn} w16^{bm} sum_a w4^{am} v[4a + b].
+template <bool INV>
+__device__ __forceinline__ void dft16(double2 (&v)[16]) {
+  constexpr double c1 = 0.92387953251128675612818318939679;  // cos(pi/8)
+  constexpr double s1 = 0.38268343236508977172845998403040;  // sin(pi/8)
+  constexpr double c2 = 0.70710678118654752440084436210485;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) dft4<INV>(v[b], v[4 + b], v[8 + b], v[12 + b]);  // v[4m + b] = u_b[m]
+  // u_b[m] *= w16^{bm} (conjugated for the inverse)
+  auto tw = [](double2 a, double wr, double wi) {
+    const double si = INV ? -wi : wi;
+    return make_double2(a.x * wr - a.y * si, a.x * si + a.y * wr);
+  };
+  v[4 * 1 + 1] = tw(v[4 * 1 + 1], c1, -s1);   // w^1
+  v[4 * 1 + 2] = tw(v[4 * 1 + 2], c2, -c2);   // w^2
+  v[4 * 1 + 3] = tw(v[4 * 1 + 3], s1, -c1);   // w^3
+  v[4 * 2 + 1] = tw(v[4 * 2 + 1], c2, -c2);   // w^2
+  v[4 * 2 + 2] = cmul_mi<INV>(v[4 * 2 + 2]);  // w^4 = -i
+  v[4 * 2 + 3] = tw(v[4 * 2 + 3], -c2, -c2);  // w^6
+  v[4 * 3 + 1] = tw(v[4 * 3 + 1], s1, -c1);   // w^3
+  v[4 * 3 + 2] = tw(v[4 * 3 + 2], -c2, -c2);  // w^6
+  v[4 * 3 + 3] = tw(v[4 * 3 + 3], -c1, s1);   // w^9
+#pragma unroll
+  for (int m = 0; m < 4; ++m) dft4<INV>(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);  // v[4m + n] = y[m + 4n]
+  double2 y[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) y[k] = v[4 * (k % 4) + k / 4];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = y[k];
+}
+
 template <int R, bool INV>
 __device__ __forceinline__ void dftR(double2 (&v)[R]) {
-  if constexpr (R == 8) {
+  if constexpr (R == 16) {
+    dft16<INV>(v);
+  } else if constexpr (R == 8) {
     dft8<INV>(v);
   } else if constexpr (R == 4) {
     dft4<INV>(v[0], v[1], v[2], v[3]);
@@ -93,17 +127,23 @@ __device__ __forceinline__ void dftR(double2 (&v)[R]) {
   }
 }
 
-template <int M>
+// Radix of the stage at sub-length M.  RULE 0: 8, then 4 / 2.  RULE 1: 16 while it divides
+// (the x2 transforms of the n >= 256 plane passes: 128 = 16 x 8, 256 = 16 x 16 -- one
+// shared-memory pass fewer than 8 x 4 x 4 / 8 x 8 x 4).
+__host__ __device__ constexpr int radix_rule(int M, int rule) {
+  return (rule == 1 && M % 16 == 0) ? 16 : ((M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2));
+}
+template <int M, int RULE = 0>
 struct Radix {
-  static constexpr int value = (M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2);
+  static constexpr int value = radix_rule(M, RULE);
 };
 
 // One in-place stage at sub-length M of a length-N transform over `npencil`
 // pencils; element e of pencil p is at buf[addr(p, e)].  Consecutive threads
 // take consecutive pencils (callers lay pencils out bank-conflict free).
-template <int N, int M, bool INV, int NP, class Addr, class TW>
-__device__ __forceinline__ void fft_stage(double2* buf, const Addr& addr, TW tw, int twstride) {
-  constexpr int R = Radix<M>::value;
+template <int N, int M, bool INV, int NP, int RULE, class Addr, class TW>
+__device__ __forceinline__ void fft_stage_r(double2* buf, const Addr& addr, TW tw, int twstride) {
+  constexpr int R = Radix<M, RULE>::value;
   constexpr int S = M / R;
   constexpr int NBF = N / R;
   constexpr int total = NP * NBF;
@@ -133,18 +173,23 @@ __device__ __forceinline__ void fft_stage(double2* buf, const Addr& addr, TW tw,
   }
 }
 
-template <int N, int M, bool INV, int NP>
+template <int N, int M, bool INV, int NP, class Addr, class TW>
+__device__ __forceinline__ void fft_stage(double2* buf, const Addr& addr, TW tw, int twstride) {
+  fft_stage_r<N, M, INV, NP, 0>(buf, addr, tw, twstride);
+}
+
+template <int N, int M, bool INV, int NP, int RULE = 0>
 struct FftRec {
   template <class Addr, class TW>
   __device__ __forceinline__ static void run(double2* buf, const Addr& addr, TW tw, int twstride) {
-    constexpr int R = Radix<M>::value;
+    constexpr int R = Radix<M, RULE>::value;
     if constexpr (!INV) {
-      fft_stage<N, M, false, NP>(buf, addr, tw, twstride);
+      fft_stage_r<N, M, false, NP, RULE>(buf, addr, tw, twstride);
       __syncthreads();
-      if constexpr (M / R > 1) FftRec<N, M / R, false, NP>::run(buf, addr, tw, twstride);
+      if constexpr (M / R > 1) FftRec<N, M / R, false, NP, RULE>::run(buf, addr, tw, twstride);
     } else {
-      if constexpr (M / R > 1) FftRec<N, M / R, true, NP>::run(buf, addr, tw, twstride);
-      fft_stage<N, M, true, NP>(buf, addr, tw, twstride);
+      if constexpr (M / R > 1) FftRec<N, M / R, true, NP, RULE>::run(buf, addr, tw, twstride);
+      fft_stage_r<N, M, true, NP, RULE>(buf, addr, tw, twstride);
       __syncthreads();
     }
   }
@@ -188,6 +233,10 @@ struct LastRadix<1> {
 template <int N, bool INV, int NP, class Addr, class TW>
 __device__ __forceinline__ void fft_smem(double2* buf, const Addr& addr, TW tw, int ntab) {
   if constexpr (N > 1) FftRec<N, N, INV, NP>::run(buf, addr, tw, ntab / N);
+}
+template <int N, bool INV, int NP, int RULE, class Addr, class TW>
+__device__ __forceinline__ void fft_smem_r(double2* buf, const Addr& addr, TW tw, int ntab) {
+  if constexpr (N > 1) FftRec<N, N, INV, NP, RULE>::run(buf, addr, tw, ntab / N);
 }
 
 // In-register in-place DIF / inverse DIT of length L on v[0..L): identical

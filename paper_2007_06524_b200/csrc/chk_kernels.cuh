@@ -190,14 +190,14 @@ struct PlanDev {
 // ----------------------------------------------------------------------------
 // digit-reversed position <-> frequency for the radix sequence of fft_smem
 // ----------------------------------------------------------------------------
-template <int N>
+template <int N, int RULE = 0>
 __device__ __forceinline__ int dig_pos(int k) {
   int p = 0;
   int M = N;
 #pragma unroll
   for (int s = 0; s < 12; ++s) {
     if (M <= 1) break;
-    const int R = (M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2);
+    const int R = radix_rule(M, RULE);
     const int m = k % R;
     k /= R;
     p += m * (M / R);
@@ -205,14 +205,14 @@ __device__ __forceinline__ int dig_pos(int k) {
   }
   return p;
 }
-template <int N>
+template <int N, int RULE = 0>
 __device__ __forceinline__ int dig_freq(int p) {
   int k = 0, mul = 1;
   int M = N;
 #pragma unroll
   for (int s = 0; s < 12; ++s) {
     if (M <= 1) break;
-    const int R = (M % 8 == 0) ? 8 : ((M % 4 == 0) ? 4 : 2);
+    const int R = radix_rule(M, RULE);
     const int Mn = M / R;
     const int m = p / Mn;
     p -= m * Mn;
@@ -251,6 +251,16 @@ __device__ __forceinline__ int dig_freq0(int p) {
   }
   return k;
 }
+
+// Radix rule of the x2 (real-FFT) transforms of the plane passes: radix 16 first at
+// n >= CHK_X2R16_MIN (half length 128 = 16 x 8, 256 = 16 x 16).
+#ifndef CHK_X2R16_MIN
+#define CHK_X2R16_MIN 256
+#endif
+template <int N>
+struct X2Rule {
+  static constexpr int value = (N >= CHK_X2R16_MIN) ? 1 : 0;
+};
 
 // ----------------------------------------------------------------------------
 // last-block reduction of two scalars per realization
@@ -832,7 +842,7 @@ __device__ __forceinline__ void r2c_post(double2* buf, int nrows, int hp, TW tw)
     const int t = i % nrows, k = i / nrows;
     double2* row = buf + t * hp;
     const int kc = (N2 - k) & (N2 - 1);
-    const int q = dig_pos<N2>(k), qc = dig_pos<N2>(kc);
+    const int q = dig_pos<N2, X2Rule<N>::value>(k), qc = dig_pos<N2, X2Rule<N>::value>(kc);
     const double2 zk = row[q];
     const double2 zc = cconj(row[qc]);
     const double2 s = cadd(zk, zc), d = csub(zk, zc);
@@ -859,7 +869,7 @@ __device__ __forceinline__ void c2r_pre(double2* buf, int nrows, int hp, TW tw) 
     const int t = i % nrows, k = i / nrows;
     double2* row = buf + t * hp;
     const int kc = (N2 - k) & (N2 - 1);
-    const int q = dig_pos<N2>(k), qc = dig_pos<N2>(kc);
+    const int q = dig_pos<N2, X2Rule<N>::value>(k), qc = dig_pos<N2, X2Rule<N>::value>(kc);
     const double2 xk = row[q];
     const double2 xc = (k == 0) ? row[N2] : row[qc];
     {
@@ -1052,7 +1062,7 @@ __device__ __forceinline__ void fwd_plane_body(const Geo& g, const double* __res
   __syncthreads();
   // R2C along x2: rows of N reals viewed as N/2 complex (z_m = x_2m + i x_2m+1)
   const PlaneTw<N> ptw = plane_tw<N>(pl);
-  fft_smem<N2, false, NR>(buf, RowAddr{HP}, ptw, N);
+  fft_smem_r<N2, false, NR, X2Rule<N>::value>(buf, RowAddr{HP}, ptw, N);
   r2c_post<N>(buf, NR, HP, ptw);
   __syncthreads();
   // C2C along the x1 group (length NR)
@@ -1179,7 +1189,7 @@ __device__ __forceinline__ void mid_slots(int c0, const PlanDev& pl, int* s_k1, 
     const int q1 = c / H, q2 = c - (c / H) * H;
     const int kp = dig_freq<NR>(q1);
     s_k1[s] = kp + m * NR;
-    const int k2 = (q2 == N2) ? N2 : dig_freq<N2>(q2);
+    const int k2 = (q2 == N2) ? N2 : dig_freq<N2, X2Rule<N>::value>(q2);
     s_k2[s] = k2;
     s_wgt[s] = (k2 == 0 || k2 == N2) ? 1.0 : 2.0;
     if (s_tw) s_tw[s] = __ldg(pl.tw + (s / W) * kp);  // as a load slot (group s/W, column w)
@@ -2069,7 +2079,7 @@ __device__ __forceinline__ void inv_plane_body(const double2* __restrict__ S, do
       if (do_u) bulk_prefetch_l2(u + ro, N * sizeof(double));
     }
     __syncthreads();
-    fft_smem<N2, true, NR>(buf, RowAddr{HP}, ptw, N);
+    fft_smem_r<N2, true, NR, X2Rule<N>::value>(buf, RowAddr{HP}, ptw, N);
   }
   double* sm = reinterpret_cast<double*>(buf);
   constexpr int Q4 = N / 4;
