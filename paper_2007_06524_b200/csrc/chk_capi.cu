@@ -2,8 +2,8 @@
 //
 // Host-side orchestration of the batched PCG (pcg_solve, solver.py:118-194):
 // init reductions, one preconditioner apply, then four kernels per iteration;
-// convergence is decided on the device, the host only polls a per-realization
-// status word every few iterations while the next iterations are already queued.
+// convergence is decided on the device, the host only polls an "any realization still
+// active" word every few iterations while the next iterations are already queued.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -1068,7 +1068,7 @@ int solve_batched_impl(const chk_grid* grid, const chk_precond_plan* plan, const
       const int chunk = (n >= 128) ? 2 : 8;
       bool pending = false;
       int ev_i = 0;
-      // poll: true when the previous chunk's status copy shows no active realization
+      // poll: stop when the previous chunk's flag shows no active realization
       auto poll = [&](int it, bool& stop) -> int {
         stop = false;
         if (it % chunk == 0 || it == opts->max_iter) {
