@@ -383,6 +383,15 @@ def generic():
         out[pre + "res"] = np.array(rep.residuals)
         out[pre + "name"] = np.array(rep.preconditioner)
         print("generic pcg", pi, cfg.n, rep.iterations, rep.converged, rep.preconditioner, rep.rhs_projected, flush=True)
+    # homogenized matrix at n = 12 (homogenize.py:92-124)
+    cfg = ch.LatticeConfig(d=3, L=3, n0=4, alpha="1/2", lam=0.1)
+    r = ch.sample_realization(cfg, 41)
+    rec = ch.homogenized_matrix(r, ch.SolveOptions(tol=1e-8, preconditioner="lkr"))
+    out["homog0_meta"] = np.array([cfg.L, cfg.n0, cfg.k, cfg.offset, 41], dtype=np.int64)
+    out["homog0_lam_tol"] = np.array([cfg.lam, 1e-8])
+    out["homog0_matrix"] = rec.matrix
+    out["homog0_its"] = np.array(rec.iterations)
+    print("generic homog", rec.iterations, flush=True)
     np.savez_compressed(os.path.join(HERE, "generic.npz"), **out)
     print("wrote generic.npz", os.path.getsize(os.path.join(HERE, "generic.npz")))
 

@@ -112,6 +112,18 @@ def test_generic_batch_matches_single_solves():
         assert torch.equal(u_seeds[m], res.u[m].cpu())
 
 
+def test_homogenized_matrix_generic():
+    """homogenize.py:92-124 at n = 12: the three corrector solves in one generic batch."""
+    g = golden_generic()
+    L, n0, k, off, seed = (int(v) for v in g["homog0_meta"])
+    lam, tol = (float(v) for v in g["homog0_lam_tol"])
+    cfg = chk.LatticeConfig(d=3, L=L, n0=n0, alpha=f"{k}/{2 * n0}", lam=lam, subcell_offset=off)
+    rec = chk.homogenized_matrix(chk.sample_realization(cfg, seed), chk.SolveOptions(tol=tol, preconditioner="lkr"))
+    assert rec.iterations == tuple(int(v) for v in g["homog0_its"])
+    ref = g["homog0_matrix"]
+    assert np.max(np.abs(rec.matrix - ref)) <= 1e-9 * np.max(np.abs(ref))
+
+
 def test_unsupported_grids_raise_value_error():
     # d = 2 and n beyond the generic path's shared-memory bound stay ValueError
     with pytest.raises(ValueError):
