@@ -56,7 +56,10 @@ def _worker(rank, P, port, q):
         for pd in pend:
             comm.finish(pd)
         planes.append(xo)
-    q.put((rank, red, out, lo, hi, planes))
+    # numpy copies: tensors through a multiprocessing queue travel as shared-memory handles
+    # served by this process, which may exit before the parent has fetched them
+    q.put((rank, red.numpy().copy(), out.numpy().copy(), lo.numpy().copy(), hi.numpy().copy(),
+           [p.numpy().copy() for p in planes]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -72,7 +75,8 @@ def test_torchcomm_matches_localcomm(P):
     got = {}
     for _ in range(P):
         r, red, out, lo, hi, planes = q.get(timeout=120)
-        got[r] = (red, out, lo, hi, planes)
+        got[r] = (torch.from_numpy(red), torch.from_numpy(out), torch.from_numpy(lo), torch.from_numpy(hi),
+                  [torch.from_numpy(p) for p in planes])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
